@@ -1,0 +1,125 @@
+/*
+ * evsim_b200.h -- C ABI of the B200-native event-camera hot path.
+ *
+ * Drop-in boundary for the reference's in-process event API
+ * (/root/reference/pkg/src/evsim/events/__init__.py:3-57).  Every entry
+ * point takes plain device pointers and sizes, is asynchronous on the given
+ * CUDA stream (a cudaStream_t passed as void*; NULL = legacy default
+ * stream), and returns an evs_status.  No torch types cross this boundary.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src):
+ *   evs_step            generate_events_parallel  evsim/events/parallel.py:126-273
+ *                       generate_events_serial    evsim/events/model.py:79-171
+ *                       (+ canonical_sort of the result, parallel.py:112-123,
+ *                        and log_transform validation, model.py:28-39)
+ *   evs_canonical_sort  canonical_sort            evsim/events/parallel.py:112-123
+ *   evs_noise           inject_noise_events       evsim/events/model.py:174-212
+ *   evs_accumulate      accumulate_events_to_image evsim/events/model.py:249-262
+ *   evs_voxel           (no reference counterpart; repo-defined voxel grid)
+ *   evs_limit_bandwidth limit_bandwidth           evsim/events/model.py:215-246
+ *   evs_seed_pcg64      numpy default_rng(seed) seeding used by
+ *                       inject_noise_events (model.py:194) -- host only
+ */
+#ifndef EVSIM_B200_H
+#define EVSIM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int evs_status;
+#define EVS_OK 0
+#define EVS_ERR_ARG 1       /* invalid argument (reference ValueError class) */
+#define EVS_ERR_CUDA 2      /* CUDA launch / runtime failure */
+#define EVS_ERR_WORKSPACE 3 /* workspace too small */
+#define EVS_ERR_UNSUPPORTED 4
+
+#define EVS_ORDER_PIXEL_MAJOR 0 /* generate_events_serial order (model.py:140-158) */
+#define EVS_ORDER_CANONICAL 1   /* (t, y, x, p) ascending (parallel.py:116) */
+
+/* Each evs_step call consumes this many consecutive epoch values. */
+#define EVS_EPOCHS_PER_CALL 8u
+/* Epochs are 22-bit; when epoch + EVS_EPOCHS_PER_CALL would exceed this,
+ * zero the workspace and restart the caller's counter at 1. */
+#define EVS_EPOCH_LIMIT ((1u << 22) - 1u)
+
+/* EventCameraConfig (types.py:129-156) + batch shape of one evs_step call:
+ * S independent sensors ("streams"), T consecutive frames per sensor. */
+typedef struct evs_step_params {
+  int32_t streams;       /* S >= 1 */
+  int32_t frames;        /* T >= 1 */
+  int32_t height;        /* H (<= 65535) */
+  int32_t width;         /* W (<= 65535) */
+  double log_eps;        /* > 0 */
+  int64_t refractory_us; /* >= 0 */
+  int64_t capacity;      /* max events kept per (stream, frame); output stride */
+  float th_pos_uniform;  /* used when th_pos == NULL (sigma_c == 0) */
+  float th_neg_uniform;
+  int64_t t0;            /* when t_bounds == NULL: frame f spans [t0+f*tick, t0+(f+1)*tick) */
+  int64_t tick;
+  int64_t max_dt;        /* upper bound of t_now - t_prev over the call (< 2^31) */
+  int32_t order;         /* EVS_ORDER_* */
+  int32_t validate;      /* 1: reject invalid frames before touching state */
+  uint32_t epoch;        /* caller-maintained counter, see EVS_EPOCHS_PER_CALL */
+  int32_t reserved;
+} evs_step_params;
+
+/* Device buffers of one evs_step call.  Segment g = s*T + f. */
+typedef struct evs_step_buffers {
+  const float* frames;     /* [S][T][H*W] intensities in [0,1] */
+  const int64_t* t_bounds; /* [S][T+1] frame timestamps (us) or NULL (t0/tick) */
+  float* ref_log;          /* [S][H*W] in/out (PixelStateGrid.ref_log) */
+  int64_t* last_event_t;   /* [S][H*W] in/out (PixelStateGrid.last_event_t) */
+  const float* th_pos;     /* [S][H*W] or NULL (uniform) */
+  const float* th_neg;     /* [S][H*W] or NULL (uniform) */
+  int64_t* ev_t;           /* [S*T][capacity] event time (us) */
+  uint16_t* ev_x;          /* [S*T][capacity] */
+  uint16_t* ev_y;          /* [S*T][capacity] */
+  int8_t* ev_p;            /* [S*T][capacity] polarity +1/-1 */
+  int64_t* counts;         /* [S*T] events written (= min(kept, capacity)) */
+  int64_t* dropped;        /* [S*T] EventBatch.dropped_count */
+  int64_t* reservations;   /* [S*T] AggregationStats.reservation_count */
+  int64_t* bad_pixel;      /* [1] must hold INT64_MAX on entry; receives the first
+                              invalid flat index into frames (s*T*H*W + f*H*W + i) */
+} evs_step_buffers;
+
+int evs_version(void);
+const char* evs_error_string(evs_status code);
+/* Bytes of device workspace evs_step needs for these params (zero-filled
+ * once by the caller; reusable across calls with the same params). */
+size_t evs_step_workspace_bytes(const evs_step_params* p);
+evs_status evs_step(const evs_step_params* p, const evs_step_buffers* b, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* evs_step that also records stage_events[i] (cudaEvent_t handles; NULL
+ * entries skipped) on `stream`: [0] before the validation prologue,
+ * [1] after it, [2] after the fused generate kernel, [3] after planning,
+ * [4] after the ordering pass(es).  Used for per-kernel roofline timing. */
+evs_status evs_step_profiled(const evs_step_params* p, const evs_step_buffers* b, void* workspace,
+                             size_t workspace_bytes, void* stream, void* const* stage_events,
+                             int32_t n_events);
+
+/* canonical_sort of one device batch of n events, in place.  Requires
+ * polarity in {-1,+1} and max(t)-min(t) < 2^31.  Workspace from
+ * evs_sort_workspace_bytes(n).  t_min/t_span from the caller (host). */
+size_t evs_sort_workspace_bytes(int64_t n, int64_t t_span);
+evs_status evs_canonical_sort(int64_t n, int64_t* t, uint16_t* x, uint16_t* y, int8_t* p,
+                              int64_t t_min, int64_t t_span, uint32_t epoch, void* workspace,
+                              size_t workspace_bytes, void* stream);
+/* batch statistics used to choose the sort path: out[0]=min t, out[1]=max t,
+ * out[2]=max x, out[3]=max y, out[4]=1 if any polarity not in {-1,+1}. */
+evs_status evs_batch_stats(int64_t n, const int64_t* t, const uint16_t* x, const uint16_t* y,
+                           const int8_t* p, int64_t* out5, void* stream);
+
+/* numpy SeedSequence(seed) -> PCG64 state (host function, no GPU).
+ * words: little-endian u32 words of the non-negative seed.
+ * out: state_hi, state_lo, inc_hi, inc_lo. */
+void evs_seed_pcg64(const uint32_t* words, int32_t nwords, uint64_t out[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EVSIM_B200_H */

@@ -1,0 +1,205 @@
+// extern "C" entry points of libevsim_b200.so (see include/evsim_b200.h).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/evsim_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace evs;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+int sm_count_current() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int cached[64] = {0};
+  if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cached[dev] = n;
+  return n;
+}
+
+struct StepLayout {
+  int nseg, ntiles1, npass, bits, NB;
+  int64_t max_tiles2;
+  size_t ctr, status1, hist, gstart, seg_total, seg_tbase, seg_tile_prefix, status2, keysA, keysB, total;
+};
+
+bool step_layout(const evs_step_params* p, StepLayout* L) {
+  if (!p || p->streams < 1 || p->frames < 1 || p->height < 1 || p->width < 1) return false;
+  if (p->height > 65535 || p->width > 65535) return false;
+  const int64_t P = (int64_t)p->height * p->width;
+  L->nseg = p->streams * p->frames;
+  L->ntiles1 = (int)((P + kGenTile - 1) / kGenTile);
+  const bool canon = p->order == EVS_ORDER_CANONICAL;
+  int tbits = 1;
+  if (canon) {
+    int64_t mdt = p->max_dt > 0 ? p->max_dt : p->tick;
+    if (mdt <= 0 || mdt >= (1ll << 31)) return false;
+    tbits = ilog2_ceil((uint64_t)mdt);
+    if (tbits < 1) tbits = 1;
+  }
+  L->npass = canon ? (tbits + kMaxDigitBits - 1) / kMaxDigitBits : 0;
+  L->bits = canon ? (tbits + L->npass - 1) / L->npass : 0;
+  L->NB = canon ? (1 << L->bits) : 0;
+  L->max_tiles2 = canon ? (p->capacity + kOrdTile - 1) / kOrdTile : 0;
+  size_t off = 0;
+  L->ctr = off; off = align_up(off + 64 * sizeof(uint32_t));
+  L->status1 = off; off = align_up(off + (size_t)L->nseg * L->ntiles1 * 8);
+  L->hist = off; off = align_up(off + (size_t)L->nseg * L->npass * kHistReps * L->NB * 4);
+  L->gstart = off; off = align_up(off + (size_t)L->nseg * L->NB * 4);
+  L->seg_total = off; off = align_up(off + (size_t)L->nseg * 8);
+  L->seg_tbase = off; off = align_up(off + (size_t)L->nseg * 8);
+  L->seg_tile_prefix = off; off = align_up(off + (size_t)(L->nseg + 1) * 4);
+  L->status2 = off; off = align_up(off + (size_t)L->nseg * L->max_tiles2 * L->NB * 8);
+  L->keysA = off; off = align_up(off + (canon ? (size_t)L->nseg * p->capacity * 8 : 0));
+  L->keysB = off; off = align_up(off + (canon && L->npass > 1 ? (size_t)L->nseg * p->capacity * 8 : 0));
+  L->total = off;
+  return true;
+}
+
+template <typename T>
+T* at(void* ws, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(ws) + off); }
+
+}  // namespace
+
+extern "C" {
+
+int evs_version(void) { return 1; }
+
+const char* evs_error_string(evs_status code) {
+  switch (code) {
+    case EVS_OK: return "ok";
+    case EVS_ERR_ARG: return "invalid argument";
+    case EVS_ERR_CUDA: return "CUDA error";
+    case EVS_ERR_WORKSPACE: return "workspace too small";
+    case EVS_ERR_UNSUPPORTED: return "unsupported input";
+    default: return "unknown error";
+  }
+}
+
+size_t evs_step_workspace_bytes(const evs_step_params* p) {
+  StepLayout L;
+  if (!step_layout(p, &L)) return 0;
+  return L.total;
+}
+
+static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b, void* ws,
+                            size_t ws_bytes, void* stream, void* const* evs, int nev) {
+  StepLayout L;
+  if (!step_layout(p, &L) || !b) return EVS_ERR_ARG;
+  if (p->log_eps <= 0 || p->refractory_us < 0 || p->capacity < 0 || p->capacity >= (1ll << 32))
+    return EVS_ERR_ARG;
+  if (!b->frames || !b->ref_log || !b->last_event_t || !b->counts || !b->dropped ||
+      !b->reservations || !b->bad_pixel)
+    return EVS_ERR_ARG;
+  if (!b->t_bounds && (p->tick <= 0 || p->tick >= (1ll << 31))) return EVS_ERR_ARG;
+  if ((b->th_pos == nullptr) != (b->th_neg == nullptr)) return EVS_ERR_ARG;
+  if (!ws || ws_bytes < L.total) return EVS_ERR_WORKSPACE;
+  if (p->epoch == 0 || p->epoch + EVS_EPOCHS_PER_CALL > EVS_EPOCH_LIMIT) return EVS_ERR_ARG;
+  const bool canon = p->order == EVS_ORDER_CANONICAL;
+  if (p->capacity > 0 && (!b->ev_t || !b->ev_x || !b->ev_y || !b->ev_p)) return EVS_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t P = (int64_t)p->height * p->width;
+
+  auto mark = [&](int i) {
+    if (evs && i < nev && evs[i]) cudaEventRecord(static_cast<cudaEvent_t>(evs[i]), st);
+  };
+  mark(0);
+  cudaError_t e = launch_prologue(b->frames, (int64_t)L.nseg * P, P, p->validate, b->bad_pixel,
+                                  b->reservations, L.nseg, st);
+  if (e != cudaSuccess) return EVS_ERR_CUDA;
+  mark(1);
+
+  GenArgs g;
+  memset(&g, 0, sizeof(g));
+  g.S = p->streams; g.T = p->frames; g.H = p->height; g.W = p->width; g.P = P;
+  g.log_eps = p->log_eps; g.refr = p->refractory_us; g.cap = p->capacity;
+  g.thp_u = p->th_pos_uniform; g.thn_u = p->th_neg_uniform;
+  g.frames = b->frames; g.t_bounds = b->t_bounds; g.t0 = p->t0; g.tick = p->tick;
+  g.ref = b->ref_log; g.last = b->last_event_t; g.thp = b->th_pos; g.thn = b->th_neg;
+  g.mode = canon ? 1 : 0;
+  g.out_t = b->ev_t; g.out_x = b->ev_x; g.out_y = b->ev_y; g.out_p = b->ev_p;
+  g.keys = canon ? at<uint64_t>(ws, L.keysA) : nullptr;
+  g.seg_stride = p->capacity;
+  g.seg_total = at<int64_t>(ws, L.seg_total);
+  g.seg_res = b->reservations;
+  g.seg_tbase = at<int64_t>(ws, L.seg_tbase);
+  g.hist = canon ? at<uint32_t>(ws, L.hist) : nullptr;
+  g.npass = L.npass; g.hist_bits = L.bits;
+  g.status = at<uint64_t>(ws, L.status1);
+  g.tile_ctr = at<uint32_t>(ws, L.ctr);
+  g.bad = b->bad_pixel;
+  g.epoch = p->epoch;
+  g.ntiles = L.ntiles1;
+  e = launch_generate(g, b->th_pos == nullptr, st);
+  if (e != cudaSuccess) return EVS_ERR_CUDA;
+  mark(2);
+
+  PlanArgs pl;
+  memset(&pl, 0, sizeof(pl));
+  pl.nseg = L.nseg; pl.cap = p->capacity; pl.seg_total = g.seg_total;
+  pl.out_count = b->counts; pl.out_dropped = b->dropped;
+  pl.hist = g.hist; pl.npass = L.npass; pl.pass = 0; pl.bits = L.bits;
+  pl.gstart = at<uint32_t>(ws, L.gstart);
+  pl.seg_tile_prefix = canon ? at<uint32_t>(ws, L.seg_tile_prefix) : nullptr;
+  pl.bad = b->bad_pixel; pl.zero_hist = 1;
+  e = launch_plan(pl, st);
+  if (e != cudaSuccess) return EVS_ERR_CUDA;
+  mark(3);
+  if (!canon) { mark(4); return EVS_OK; }
+
+  if (L.npass > 1) {
+    HistArgs h;
+    h.nseg = L.nseg; h.keys = g.keys; h.seg_stride = p->capacity; h.seg_count = b->counts;
+    h.npass = L.npass; h.pass0 = 1; h.bits = L.bits; h.base_shift = kKeyPixBits; h.hist = g.hist;
+    e = launch_hist(h, st);
+    if (e != cudaSuccess) return EVS_ERR_CUDA;
+  }
+  const int sms = sm_count_current();
+  for (int pass = 0; pass < L.npass; ++pass) {
+    if (pass > 0) {
+      PlanArgs p2 = pl;
+      p2.out_count = nullptr; p2.out_dropped = nullptr; p2.pass = pass; p2.seg_tile_prefix = nullptr;
+      e = launch_plan(p2, st);
+      if (e != cudaSuccess) return EVS_ERR_CUDA;
+    }
+    OrderArgs o;
+    memset(&o, 0, sizeof(o));
+    o.nseg = L.nseg;
+    o.keys_in = (pass % 2 == 0) ? at<uint64_t>(ws, L.keysA) : at<uint64_t>(ws, L.keysB);
+    o.keys_out = (pass % 2 == 0) ? at<uint64_t>(ws, L.keysB) : at<uint64_t>(ws, L.keysA);
+    o.seg_stride = p->capacity; o.seg_count = b->counts;
+    o.seg_tile_prefix = at<uint32_t>(ws, L.seg_tile_prefix);
+    o.gstart = pl.gstart; o.shift = kKeyPixBits + pass * L.bits; o.bits = L.bits;
+    o.status = at<uint64_t>(ws, L.status2); o.max_tiles = L.max_tiles2;
+    o.ctr = at<uint32_t>(ws, L.ctr) + 1 + pass; o.epoch = p->epoch + 1 + pass;
+    o.final_soa = pass == L.npass - 1;
+    o.out_t = b->ev_t; o.out_x = b->ev_x; o.out_y = b->ev_y; o.out_p = b->ev_p;
+    o.seg_tbase = g.seg_tbase;
+    e = launch_order(o, sms, st);
+    if (e != cudaSuccess) return EVS_ERR_CUDA;
+  }
+  mark(4);
+  return EVS_OK;
+}
+
+evs_status evs_step(const evs_step_params* p, const evs_step_buffers* b, void* ws, size_t ws_bytes,
+                    void* stream) {
+  return step_impl(p, b, ws, ws_bytes, stream, nullptr, 0);
+}
+
+evs_status evs_step_profiled(const evs_step_params* p, const evs_step_buffers* b, void* ws,
+                             size_t ws_bytes, void* stream, void* const* stage_events,
+                             int32_t n_events) {
+  return step_impl(p, b, ws, ws_bytes, stream, stage_events, n_events);
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// Kernel argument blocks and launch helpers shared by the .cu files.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace evs {
+
+constexpr int64_t kNoBad = 0x7fffffffffffffffLL;
+constexpr int kHistReps = 8;      // replicated global histograms (atomic spread)
+constexpr int kMaxDigitBits = 11; // onesweep digit width (<= 2048 bins)
+constexpr int kKeyPixBits = 33;   // key = t_rel << 33 | y << 17 | x << 1 | (p > 0)
+
+constexpr int kGenThreads = 256;
+constexpr int kGenVpt = 4;
+constexpr int kGenTile = kGenThreads * kGenVpt;  // pixels per K1 tile
+constexpr int kGenStage = 4 * kGenTile;          // staged keys per tile (smem)
+
+constexpr int kOrdThreads = 256;
+constexpr int kOrdIpt = 16;
+constexpr int kOrdTile = kOrdThreads * kOrdIpt;  // keys per K2 tile
+
+struct GenArgs {
+  int S, T, H, W;
+  int64_t P;
+  double log_eps;
+  int64_t refr, cap;
+  float thp_u, thn_u;
+  const float* frames;      // [S][T][P]
+  const int64_t* t_bounds;  // [S][T+1] or null
+  int64_t t0, tick;
+  float* ref;
+  int64_t* last;
+  const float* thp;
+  const float* thn;
+  int mode;  // 0: SoA pixel-major, 1: keys to scratch
+  int64_t* out_t;
+  uint16_t* out_x;
+  uint16_t* out_y;
+  int8_t* out_p;
+  uint64_t* keys;
+  int64_t seg_stride;
+  int64_t* seg_total;  // [S*T] kept events before capacity
+  int64_t* seg_res;    // [S*T] reservation chunks
+  int64_t* seg_tbase;  // [S*T] t_prev of each segment
+  uint32_t* hist;      // [S*T][npass][R][NB] (pass 0) or null
+  int npass, hist_bits;
+  uint64_t* status;  // [S*T][ntiles]
+  uint32_t* tile_ctr;
+  const int64_t* bad;
+  uint32_t epoch;
+  int ntiles;  // tiles per stream frame
+};
+
+struct PlanArgs {
+  int nseg;
+  int64_t cap;
+  const int64_t* seg_total;
+  int64_t* out_count;
+  int64_t* out_dropped;
+  const uint32_t* hist;  // [nseg][npass][R][NB] or null
+  int npass, pass, bits;
+  uint32_t* gstart;           // [nseg][NB]
+  uint32_t* seg_tile_prefix;  // [nseg+1]
+  const int64_t* bad;
+  int zero_hist;
+};
+
+struct OrderArgs {
+  int nseg;
+  const uint64_t* keys_in;
+  int64_t seg_stride;
+  const int64_t* seg_count;
+  const uint32_t* seg_tile_prefix;
+  const uint32_t* gstart;
+  int shift, bits;
+  uint64_t* status;  // [nseg][max_tiles][NB]
+  int64_t max_tiles;
+  uint32_t* ctr;
+  uint32_t epoch;
+  int final_soa;
+  uint64_t* keys_out;
+  int64_t* out_t;
+  uint16_t* out_x;
+  uint16_t* out_y;
+  int8_t* out_p;
+  const int64_t* seg_tbase;
+};
+
+struct HistArgs {
+  int nseg;
+  const uint64_t* keys;
+  int64_t seg_stride;
+  const int64_t* seg_count;
+  int npass, pass0, bits;  // histogram passes [pass0, npass)
+  int base_shift;          // bit position of pass 0's digit
+  uint32_t* hist;          // [nseg][npass][R][NB]
+};
+
+// host launchers (kernels.cu)
+cudaError_t launch_prologue(const float* frames, int64_t nframes, int64_t P, int validate,
+                            int64_t* bad, int64_t* seg_res, int nseg, cudaStream_t st);
+cudaError_t launch_generate(const GenArgs& a, int uniform_th, cudaStream_t st);
+cudaError_t launch_plan(const PlanArgs& a, cudaStream_t st);
+cudaError_t launch_hist(const HistArgs& a, cudaStream_t st);
+cudaError_t launch_order(const OrderArgs& a, int sm_count, cudaStream_t st);
+
+}  // namespace evs

@@ -1,0 +1,137 @@
+"""Host runtime around the C ABI: workspaces, output pools, epochs, streams.
+
+``StepEngine`` owns everything one ``evs_step`` shape needs (device
+workspace, padded per-segment output pool, per-segment counters) so repeated
+calls allocate nothing.  All work is enqueued on the caller's CUDA stream;
+nothing here synchronises except the explicit ``fetch_*`` helpers.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+
+@dataclass(frozen=True)
+class StepShape:
+    streams: int
+    frames: int
+    height: int
+    width: int
+    capacity: int
+    order: int
+    max_dt: int
+    log_eps: float
+    refractory_us: int
+    uniform: tuple | None  # (th_pos, th_neg) or None
+
+
+class StepEngine:
+    """Reusable launch context for one StepShape (one sensor group)."""
+
+    def __init__(self, shape: StepShape, device):
+        import torch
+
+        _lib.require_cuda()
+        self.shape = shape
+        self.device = device
+        self.lib = _lib.load()
+        self.params = _lib.StepParams()
+        p = self.params
+        p.streams, p.frames = shape.streams, shape.frames
+        p.height, p.width = shape.height, shape.width
+        p.log_eps = float(shape.log_eps)
+        p.refractory_us = int(shape.refractory_us)
+        p.capacity = int(shape.capacity)
+        if shape.uniform is not None:
+            p.th_pos_uniform, p.th_neg_uniform = shape.uniform
+        p.max_dt = int(shape.max_dt)
+        p.order = int(shape.order)
+        p.validate = 1
+        nbytes = self.lib.evs_step_workspace_bytes(ctypes.byref(p))
+        if nbytes == 0:
+            raise ValueError(f"unsupported step shape {shape}")
+        self.workspace = torch.zeros(int(nbytes), dtype=torch.uint8, device=device)
+        nseg = shape.streams * shape.frames
+        cap = max(int(shape.capacity), 1)
+        self.ev_t = torch.empty((nseg, cap), dtype=torch.int64, device=device)
+        self.ev_x = torch.empty((nseg, cap), dtype=torch.int16, device=device)
+        self.ev_y = torch.empty((nseg, cap), dtype=torch.int16, device=device)
+        self.ev_p = torch.empty((nseg, cap), dtype=torch.int8, device=device)
+        # info rows: counts, dropped, reservations ; bad pixel in a separate slot
+        self.info = torch.zeros((3, nseg), dtype=torch.int64, device=device)
+        self.bad = torch.full((1,), _lib.NO_BAD, dtype=torch.int64, device=device)
+        self.epochs = _lib.EpochCounter()
+        self.bufs = _lib.StepBuffers()
+
+    def launch(self, frames, ref_log, last_event_t, th_pos=None, th_neg=None, t_bounds=None,
+               t0: int = 0, tick: int = 0, validate: bool = True, stream=None,
+               stage_events=None) -> None:
+        """Enqueue one evs_step on `stream` (default: torch's current stream).
+
+        stage_events: optional list of 5 torch.cuda.Event(enable_timing=True)
+        recorded around the prologue / generate / plan / order stages.
+        """
+        p, b = self.params, self.bufs
+        p.t0, p.tick = int(t0), int(tick)
+        p.validate = 1 if validate else 0
+        p.epoch = self.epochs.take(self.workspace)
+        b.frames = frames.data_ptr()
+        b.t_bounds = t_bounds.data_ptr() if t_bounds is not None else None
+        b.ref_log = ref_log.data_ptr()
+        b.last_event_t = last_event_t.data_ptr()
+        if self.shape.uniform is None:
+            b.th_pos, b.th_neg = th_pos.data_ptr(), th_neg.data_ptr()
+        else:
+            b.th_pos = b.th_neg = None
+        b.ev_t, b.ev_x = self.ev_t.data_ptr(), self.ev_x.data_ptr()
+        b.ev_y, b.ev_p = self.ev_y.data_ptr(), self.ev_p.data_ptr()
+        b.counts = self.info[0].data_ptr()
+        b.dropped = self.info[1].data_ptr()
+        b.reservations = self.info[2].data_ptr()
+        b.bad_pixel = self.bad.data_ptr()
+        ws = ctypes.c_void_p(self.workspace.data_ptr())
+        nb = ctypes.c_size_t(self.workspace.numel())
+        sp = ctypes.c_void_p(_lib.stream_ptr(stream))
+        if stage_events is None:
+            rc = self.lib.evs_step(ctypes.byref(p), ctypes.byref(b), ws, nb, sp)
+        else:
+            handles = (ctypes.c_void_p * len(stage_events))(*[e.cuda_event for e in stage_events])
+            rc = self.lib.evs_step_profiled(ctypes.byref(p), ctypes.byref(b), ws, nb, sp, handles,
+                                            len(stage_events))
+        _lib.check(rc, "evs_step")
+
+    def fetch_info(self):
+        """Synchronising read of (counts, dropped, reservations, bad)."""
+        import torch
+
+        host = torch.cat([self.info.reshape(-1), self.bad]).cpu().numpy()
+        nseg = self.info.shape[1]
+        return host[:nseg], host[nseg:2 * nseg], host[2 * nseg:3 * nseg], int(host[-1])
+
+    def reset_bad(self) -> None:
+        self.bad.fill_(_lib.NO_BAD)
+
+
+def upload_frame(values, device, staging_cache: dict | None = None):
+    """Host numpy (H, W) float32 -> device tensor (via a cached pinned buffer)."""
+    import torch
+
+    if type(values).__module__.startswith("torch"):
+        return values.to(device=device, dtype=torch.float32).contiguous()
+    arr = np.ascontiguousarray(values, np.float32)
+    if staging_cache is not None:
+        key = ("stage", arr.shape)
+        pin = staging_cache.get(key)
+        if pin is None:
+            pin = torch.empty(arr.shape, dtype=torch.float32, pin_memory=True)
+            staging_cache[key] = pin
+        pin.numpy()[...] = arr
+        out = torch.empty(arr.shape, dtype=torch.float32, device=device)
+        out.copy_(pin, non_blocking=True)
+        return out
+    return torch.from_numpy(arr).to(device)
