@@ -246,6 +246,14 @@ def run_ours(args):
     counts, _, _, _ = eng.fetch_info()
     E_step = int(counts.sum())
 
+    # CUDA graph of G steps (one per ring window); the step clock advances on
+    # the device so replays continue the frame sequence.  K = R * G exactly.
+    G = max(g for g in range(1, min(K, 64) + 1) if K % g == 0 and (g % len(windows) == 0 or g < len(windows)))
+    k_next = state["k"]
+    graph_windows = [windows[(k_next + i) % len(windows)] for i in range(G)]
+    eng.capture(graph_windows, st.d_ref_log, st.d_last_event_t, tick=TICK, t0=k_next * T * TICK)
+    reps = K // G
+
     sampler = ClockSampler(local)
     if world > 1:
         dist.barrier()
@@ -254,12 +262,15 @@ def run_ours(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(K):
-        step()
+    for _ in range(reps):
+        eng.replay()
     e1.record(stream)
     torch.cuda.synchronize()
     sampler.stop()
     ms = e0.elapsed_time(e1)
+    state["k"] = k_next + K
+    counts, dropped, _, bad = eng.fetch_info()
+    assert bad == _lib.NO_BAD and int(dropped.sum()) == 0
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -339,7 +350,7 @@ def run_ours(args):
                                        "frac": gen_achieved / peak}},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": K * 4,
+        "gpu_launches": K * 4 + reps,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

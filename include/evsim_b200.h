@@ -64,8 +64,14 @@ typedef struct evs_step_params {
   int32_t order;         /* EVS_ORDER_* */
   int32_t validate;      /* 1: reject invalid frames before touching state */
   uint32_t epoch;        /* caller-maintained counter, see EVS_EPOCHS_PER_CALL */
-  int32_t reserved;
+  int32_t flags;         /* EVS_FLAG_* */
 } evs_step_params;
+
+/* flags: t0 and epoch are taken from a clock kept in the workspace and
+ * advanced on the device by every step (t0 += frames*tick, epoch += 8), so a
+ * captured CUDA graph of evs_step calls can be replayed.  Initialise it with
+ * evs_step_clock_init; params.t0 / params.epoch are then ignored. */
+#define EVS_FLAG_DEVICE_CLOCK 1
 
 /* Device buffers of one evs_step call.  Segment g = s*T + f. */
 typedef struct evs_step_buffers {
@@ -93,6 +99,10 @@ const char* evs_error_string(evs_status code);
 size_t evs_step_workspace_bytes(const evs_step_params* p);
 evs_status evs_step(const evs_step_params* p, const evs_step_buffers* b, void* workspace,
                     size_t workspace_bytes, void* stream);
+/* Set the device clock of a workspace (EVS_FLAG_DEVICE_CLOCK): the next step
+ * starts at t0 and uses epoch (asynchronous on stream). */
+evs_status evs_step_clock_init(const evs_step_params* p, void* workspace, size_t workspace_bytes,
+                               int64_t t0, uint32_t epoch, void* stream);
 
 /* evs_step that also records stage_events[i] (cudaEvent_t handles; NULL
  * entries skipped) on `stream`: [0] before the validation prologue,

@@ -27,6 +27,7 @@ NO_BAD = 0x7FFFFFFFFFFFFFFF
 # Every symbol include/evsim_b200.h declares (checked by tests/test_capi_symbols.py).
 EXPORTED_SYMBOLS = (
     "evs_version", "evs_error_string", "evs_step_workspace_bytes", "evs_step",
+    "evs_step_profiled", "evs_step_clock_init",
     "evs_sort_workspace_bytes", "evs_canonical_sort", "evs_batch_stats", "evs_seed_pcg64",
     "evs_noise_workspace_bytes", "evs_noise", "evs_accumulate", "evs_voxel",
     "evs_limit_bandwidth_workspace_bytes", "evs_limit_bandwidth",
@@ -42,8 +43,11 @@ class StepParams(ctypes.Structure):
         ("th_pos_uniform", ctypes.c_float), ("th_neg_uniform", ctypes.c_float),
         ("t0", ctypes.c_int64), ("tick", ctypes.c_int64), ("max_dt", ctypes.c_int64),
         ("order", ctypes.c_int32), ("validate", ctypes.c_int32),
-        ("epoch", ctypes.c_uint32), ("reserved", ctypes.c_int32),
+        ("epoch", ctypes.c_uint32), ("flags", ctypes.c_int32),
     ]
+
+
+EVS_FLAG_DEVICE_CLOCK = 1
 
 
 class StepBuffers(ctypes.Structure):
@@ -94,6 +98,7 @@ def load():
         L.evs_step.argtypes = [ctypes.POINTER(StepParams), ctypes.POINTER(StepBuffers), P, sz, P]
         L.evs_step_profiled.argtypes = [ctypes.POINTER(StepParams), ctypes.POINTER(StepBuffers), P, sz,
                                         P, P, ctypes.c_int32]
+        L.evs_step_clock_init.argtypes = [ctypes.POINTER(StepParams), P, sz, i64, u32, P]
         L.evs_sort_workspace_bytes.restype = sz
         L.evs_sort_workspace_bytes.argtypes = [i64, i64]
         L.evs_canonical_sort.argtypes = [i64, P, P, P, P, i64, i64, u32, P, sz, P]

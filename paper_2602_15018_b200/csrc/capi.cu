@@ -29,8 +29,16 @@ int sm_count_current() {
 struct StepLayout {
   int nseg, ntiles1, npass, bits, NB;
   int64_t max_tiles2;
-  size_t ctr, status1, hist, gstart, seg_total, seg_tbase, seg_tile_prefix, status2, keysA, keysB, total;
+  size_t ctr, desc, status1, hist, gstart, seg_total, seg_tbase, seg_tile_prefix, status2, keysA, keysB,
+      total;
 };
+
+__global__ void k_clock_init(StepDesc* d, int64_t t0, uint32_t epoch) {
+  d->next_t0 = t0;
+  d->cur_t0 = t0;
+  d->next_epoch = epoch;
+  d->cur_epoch = epoch;
+}
 
 bool step_layout(const evs_step_params* p, StepLayout* L) {
   if (!p || p->streams < 1 || p->frames < 1 || p->height < 1 || p->width < 1) return false;
@@ -52,6 +60,7 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   L->max_tiles2 = canon ? (p->capacity + kOrdTile - 1) / kOrdTile : 0;
   size_t off = 0;
   L->ctr = off; off = align_up(off + 64 * sizeof(uint32_t));
+  L->desc = off; off = align_up(off + sizeof(StepDesc));
   L->status1 = off; off = align_up(off + (size_t)L->nseg * L->ntiles1 * 8);
   L->hist = off; off = align_up(off + (size_t)L->nseg * L->npass * kHistReps * L->NB * 4);
   L->gstart = off; off = align_up(off + (size_t)L->nseg * L->NB * 4);
@@ -103,7 +112,10 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   if (!b->t_bounds && (p->tick <= 0 || p->tick >= (1ll << 31))) return EVS_ERR_ARG;
   if ((b->th_pos == nullptr) != (b->th_neg == nullptr)) return EVS_ERR_ARG;
   if (!ws || ws_bytes < L.total) return EVS_ERR_WORKSPACE;
-  if (p->epoch == 0 || p->epoch + EVS_EPOCHS_PER_CALL > EVS_EPOCH_LIMIT) return EVS_ERR_ARG;
+  const bool dclock = (p->flags & EVS_FLAG_DEVICE_CLOCK) != 0;
+  if (!dclock && (p->epoch == 0 || p->epoch + EVS_EPOCHS_PER_CALL > EVS_EPOCH_LIMIT)) return EVS_ERR_ARG;
+  if (dclock && b->t_bounds) return EVS_ERR_ARG;
+  StepDesc* desc = dclock ? at<StepDesc>(ws, L.desc) : nullptr;
   const bool canon = p->order == EVS_ORDER_CANONICAL;
   if (p->capacity > 0 && (!b->ev_t || !b->ev_x || !b->ev_y || !b->ev_p)) return EVS_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -114,7 +126,7 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   };
   mark(0);
   cudaError_t e = launch_prologue(b->frames, (int64_t)L.nseg * P, P, p->validate, b->bad_pixel,
-                                  b->reservations, L.nseg, st);
+                                  b->reservations, L.nseg, desc, (int64_t)p->frames * p->tick, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(1);
 
@@ -139,6 +151,7 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   g.bad = b->bad_pixel;
   g.epoch = p->epoch;
   g.ntiles = L.ntiles1;
+  g.desc = desc;
   e = launch_generate(g, b->th_pos == nullptr, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(2);
@@ -180,7 +193,9 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
     o.seg_tile_prefix = at<uint32_t>(ws, L.seg_tile_prefix);
     o.gstart = pl.gstart; o.shift = kKeyPixBits + pass * L.bits; o.bits = L.bits;
     o.status = at<uint64_t>(ws, L.status2); o.max_tiles = L.max_tiles2;
-    o.ctr = at<uint32_t>(ws, L.ctr) + 1 + pass; o.epoch = p->epoch + 1 + pass;
+    o.ctr = at<uint32_t>(ws, L.ctr) + 1 + pass;
+    o.epoch = dclock ? (uint32_t)(1 + pass) : p->epoch + 1 + pass;
+    o.desc = desc;
     o.final_soa = pass == L.npass - 1;
     o.out_t = b->ev_t; o.out_x = b->ev_x; o.out_y = b->ev_y; o.out_p = b->ev_p;
     o.seg_tbase = g.seg_tbase;
@@ -194,6 +209,16 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
 evs_status evs_step(const evs_step_params* p, const evs_step_buffers* b, void* ws, size_t ws_bytes,
                     void* stream) {
   return step_impl(p, b, ws, ws_bytes, stream, nullptr, 0);
+}
+
+evs_status evs_step_clock_init(const evs_step_params* p, void* ws, size_t ws_bytes, int64_t t0,
+                               uint32_t epoch, void* stream) {
+  StepLayout L;
+  if (!step_layout(p, &L)) return EVS_ERR_ARG;
+  if (!ws || ws_bytes < L.total) return EVS_ERR_WORKSPACE;
+  if (epoch == 0 || epoch + EVS_EPOCHS_PER_CALL > EVS_EPOCH_LIMIT) return EVS_ERR_ARG;
+  k_clock_init<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(at<StepDesc>(ws, L.desc), t0, epoch);
+  return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
 }
 
 evs_status evs_step_profiled(const evs_step_params* p, const evs_step_buffers* b, void* ws,

@@ -30,9 +30,16 @@ namespace evs {
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_prologue(const float* __restrict__ frames, int64_t n,
                                                   int validate, int64_t* bad, int64_t* seg_res,
-                                                  int nseg) {
-  if (blockIdx.x == 0)
+                                                  int nseg, StepDesc* desc, int64_t t_advance) {
+  if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < nseg; i += blockDim.x) seg_res[i] = 0;
+    if (desc && threadIdx.x == 0) {  // advance the device clock for this step
+      desc->cur_t0 = desc->next_t0;
+      desc->next_t0 += t_advance;
+      desc->cur_epoch = desc->next_epoch;
+      desc->next_epoch += 8u;
+    }
+  }
   if (!validate) return;
   int64_t first = kNoBad;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -64,7 +71,8 @@ __global__ void __launch_bounds__(256) k_prologue(const float* __restrict__ fram
 }
 
 cudaError_t launch_prologue(const float* frames, int64_t nframes_px, int64_t P, int validate,
-                            int64_t* bad, int64_t* seg_res, int nseg, cudaStream_t st) {
+                            int64_t* bad, int64_t* seg_res, int nseg, StepDesc* desc,
+                            int64_t t_advance, cudaStream_t st) {
   (void)P;
   int64_t work = validate ? (nframes_px + 3) / 4 : 1;
   int64_t blocks = (work + 255) / 256;
@@ -72,9 +80,11 @@ cudaError_t launch_prologue(const float* frames, int64_t nframes_px, int64_t P, 
   if (blocks < 1) blocks = 1;
   bool vec = ((uintptr_t)frames % 16) == 0;
   if (vec)
-    k_prologue<true><<<(unsigned)blocks, 256, 0, st>>>(frames, nframes_px, validate, bad, seg_res, nseg);
+    k_prologue<true><<<(unsigned)blocks, 256, 0, st>>>(frames, nframes_px, validate, bad, seg_res, nseg,
+                                                       desc, t_advance);
   else
-    k_prologue<false><<<(unsigned)blocks, 256, 0, st>>>(frames, nframes_px, validate, bad, seg_res, nseg);
+    k_prologue<false><<<(unsigned)blocks, 256, 0, st>>>(frames, nframes_px, validate, bad, seg_res, nseg,
+                                                        desc, t_advance);
   return cudaGetLastError();
 }
 
@@ -127,6 +137,8 @@ __global__ void __launch_bounds__(kGenThreads, 3) k_generate(GenArgs a) {
   const int s = (int)(id / (uint32_t)a.ntiles);
   const int tile = (int)(id % (uint32_t)a.ntiles);
   const int64_t P = a.P;
+  const uint32_t epoch = a.desc ? a.desc->cur_epoch : a.epoch;
+  const int64_t clock_t0 = a.desc ? a.desc->cur_t0 : a.t0;
   const int64_t pix0 = (int64_t)tile * TILE + (int64_t)tid * VPT;
   const bool full = VEC && (pix0 + VPT <= P);
   float* refp = a.ref + (int64_t)s * P;
@@ -169,7 +181,7 @@ __global__ void __launch_bounds__(kGenThreads, 3) k_generate(GenArgs a) {
       tprev = a.t_bounds[(int64_t)s * (a.T + 1) + f];
       tnow = a.t_bounds[(int64_t)s * (a.T + 1) + f + 1];
     } else {
-      tprev = a.t0 + (int64_t)f * a.tick;
+      tprev = clock_t0 + (int64_t)f * a.tick;
       tnow = tprev + a.tick;
     }
     const int64_t dt = tnow - tprev;
@@ -247,11 +259,11 @@ __global__ void __launch_bounds__(kGenThreads, 3) k_generate(GenArgs a) {
       uint64_t* st = a.status + (int64_t)seg * a.ntiles;
       uint64_t ex = 0;
       if (tile == 0) {
-        if (lane == 0) st_relaxed(st, pack_status(kFlagInc, a.epoch, (uint64_t)tile_total));
+        if (lane == 0) st_relaxed(st, pack_status(kFlagInc, epoch, (uint64_t)tile_total));
       } else {
-        if (lane == 0) st_relaxed(st + tile, pack_status(kFlagAgg, a.epoch, (uint64_t)tile_total));
-        ex = warp_lookback(st, tile, a.epoch);
-        if (lane == 0) st_relaxed(st + tile, pack_status(kFlagInc, a.epoch, ex + (uint64_t)tile_total));
+        if (lane == 0) st_relaxed(st + tile, pack_status(kFlagAgg, epoch, (uint64_t)tile_total));
+        ex = warp_lookback(st, tile, epoch);
+        if (lane == 0) st_relaxed(st + tile, pack_status(kFlagInc, epoch, ex + (uint64_t)tile_total));
       }
       if (lane == 0) {
         s_base = (int64_t)ex;
@@ -316,15 +328,28 @@ __global__ void __launch_bounds__(kGenThreads, 3) k_generate(GenArgs a) {
   }
 }
 
+// Raise a kernel's dynamic-smem limit once per process (not per launch).
+template <typename K>
+static void ensure_smem(K k, size_t smem) {
+  static const void* done[64];
+  static int ndone = 0;
+  if (smem <= 48 * 1024) return;
+  const void* key = reinterpret_cast<const void*>(k);
+  for (int i = 0; i < ndone; ++i)
+    if (done[i] == key) return;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (ndone < 64) done[ndone++] = key;
+}
+
 template <bool VEC, bool REFR, bool UNI>
 static cudaError_t gen_dispatch_mode(const GenArgs& a, unsigned grid, size_t smem, cudaStream_t st) {
   if (a.mode == 0) {
     auto k = k_generate<VEC, REFR, UNI, 0>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(k, smem);
     k<<<grid, kGenThreads, smem, st>>>(a);
   } else {
     auto k = k_generate<VEC, REFR, UNI, 1>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(k, smem);
     k<<<grid, kGenThreads, smem, st>>>(a);
   }
   return cudaGetLastError();
@@ -447,7 +472,7 @@ cudaError_t launch_hist(const HistArgs& a, cudaStream_t st) {
   const int NB = 1 << a.bits;
   const size_t smem = (size_t)(a.npass - a.pass0) * NB * 4;
   dim3 grid(64, a.nseg);
-  cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem(k_hist, smem);
   k_hist<<<grid, 256, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -468,6 +493,7 @@ __global__ void __launch_bounds__(kOrdThreads) k_order(OrderArgs a) {
   __shared__ uint32_t s_scan[NW + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t dmask = (uint64_t)(NB - 1);
+  const uint32_t epoch = a.desc ? a.desc->cur_epoch + a.epoch : a.epoch;
 
   for (;;) {
     const uint32_t total = a.seg_tile_prefix[a.nseg];
@@ -550,7 +576,7 @@ __global__ void __launch_bounds__(kOrdThreads) k_order(OrderArgs a) {
         ex[j] = 0; jj[j] = tile - 1; tb[j] = 0;
         if (d < NB) {
           tb[j] = gbase[d];
-          st_relaxed(stt + tile * NB + d, pack_status(tile == 0 ? kFlagInc : kFlagAgg, a.epoch, tb[j]));
+          st_relaxed(stt + tile * NB + d, pack_status(tile == 0 ? kFlagInc : kFlagAgg, epoch, tb[j]));
         }
       }
       if (tile > 0) {
@@ -567,7 +593,7 @@ __global__ void __launch_bounds__(kOrdThreads) k_order(OrderArgs a) {
           for (int j = 0; j < MAXPER; ++j) {
             const int d = tid + j * NT;
             if (d < NB && jj[j] >= 0) {
-              const uint32_t fl = status_flag(wv[j], a.epoch);
+              const uint32_t fl = status_flag(wv[j], epoch);
               if (fl == 0) { pending = true; continue; }
               ex[j] += status_value(wv[j]);
               jj[j] = (fl == kFlagInc) ? -1 : jj[j] - 1;
@@ -578,7 +604,7 @@ __global__ void __launch_bounds__(kOrdThreads) k_order(OrderArgs a) {
 #pragma unroll
         for (int j = 0; j < MAXPER; ++j) {
           const int d = tid + j * NT;
-          if (d < NB) st_relaxed(stt + tile * NB + d, pack_status(kFlagInc, a.epoch, ex[j] + tb[j]));
+          if (d < NB) st_relaxed(stt + tile * NB + d, pack_status(kFlagInc, epoch, ex[j] + tb[j]));
         }
       }
 #pragma unroll
@@ -622,10 +648,15 @@ __global__ void __launch_bounds__(kOrdThreads) k_order(OrderArgs a) {
 cudaError_t launch_order(const OrderArgs& a, int sm_count, cudaStream_t st) {
   const int NB = 1 << a.bits;
   const size_t smem = (size_t)kOrdTile * 8 + (size_t)(kOrdThreads / 32) * NB * 2 + (size_t)NB * 8;
-  cudaFuncSetAttribute(k_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_order, kOrdThreads, smem);
-  if (per_sm < 1) per_sm = 1;
+  ensure_smem(k_order, smem);
+  // occupancy per digit width, cached (the query is slow relative to a launch)
+  static int occ_cache[kMaxDigitBits + 1] = {0};
+  int per_sm = occ_cache[a.bits];
+  if (per_sm == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_order, kOrdThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    occ_cache[a.bits] = per_sm;
+  }
   k_order<<<sm_count * per_sm, kOrdThreads, smem, st>>>(a);
   return cudaGetLastError();
 }

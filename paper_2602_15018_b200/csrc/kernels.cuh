@@ -19,6 +19,13 @@ constexpr int kOrdThreads = 256;
 constexpr int kOrdIpt = 16;
 constexpr int kOrdTile = kOrdThreads * kOrdIpt;  // keys per K2 tile
 
+// Device-resident step clock (EVS_FLAG_DEVICE_CLOCK): lets a captured CUDA
+// graph replay steps whose start time and lookback epoch advance on device.
+struct StepDesc {
+  int64_t next_t0, cur_t0;
+  uint32_t next_epoch, cur_epoch;
+};
+
 struct GenArgs {
   int S, T, H, W;
   int64_t P;
@@ -49,6 +56,7 @@ struct GenArgs {
   const int64_t* bad;
   uint32_t epoch;
   int ntiles;  // tiles per stream frame
+  const StepDesc* desc;  // non-null: t0 / epoch come from the device clock
 };
 
 struct PlanArgs {
@@ -84,6 +92,7 @@ struct OrderArgs {
   uint16_t* out_y;
   int8_t* out_p;
   const int64_t* seg_tbase;
+  const StepDesc* desc;  // non-null: epoch = desc->cur_epoch + epoch
 };
 
 struct HistArgs {
@@ -98,7 +107,8 @@ struct HistArgs {
 
 // host launchers (kernels.cu)
 cudaError_t launch_prologue(const float* frames, int64_t nframes, int64_t P, int validate,
-                            int64_t* bad, int64_t* seg_res, int nseg, cudaStream_t st);
+                            int64_t* bad, int64_t* seg_res, int nseg, StepDesc* desc,
+                            int64_t t_advance, cudaStream_t st);
 cudaError_t launch_generate(const GenArgs& a, int uniform_th, cudaStream_t st);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t st);
 cudaError_t launch_hist(const HistArgs& a, cudaStream_t st);

@@ -68,9 +68,12 @@ __global__ void __launch_bounds__(256) k_pack(int64_t n, const int64_t* __restri
                                               const uint16_t* __restrict__ x,
                                               const uint16_t* __restrict__ y,
                                               const int8_t* __restrict__ p, int64_t t_min,
-                                              uint64_t* keys, int64_t* meta) {
+                                              uint64_t* keys, int64_t* meta, uint32_t* hist,
+                                              int64_t hist_words) {
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i0 == 0) { meta[0] = n; meta[1] = t_min; meta[2] = kNoBad; }
+  // the workspace may be reused with another layout: clear the histogram region
+  for (int64_t i = i0; i < hist_words; i += (int64_t)gridDim.x * blockDim.x) hist[i] = 0;
   for (int64_t i = i0; i < n; i += (int64_t)gridDim.x * blockDim.x)
     keys[i] = ((uint64_t)(t[i] - t_min) << kKeyPixBits) | ((uint64_t)y[i] << 17) |
               ((uint64_t)x[i] << 1) | (p[i] > 0 ? 1u : 0u);
@@ -150,7 +153,8 @@ evs_status evs_canonical_sort(int64_t n, int64_t* t, uint16_t* x, uint16_t* y, i
   uint64_t* kB = at<uint64_t>(ws, L.keysB);
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_pack<<<(unsigned)blocks, 256, 0, st>>>(n, t, x, y, p, t_min, kA, meta);
+  k_pack<<<(unsigned)blocks, 256, 0, st>>>(n, t, x, y, p, t_min, kA, meta, at<uint32_t>(ws, L.hist),
+                                           (int64_t)L.npass * kHistReps * L.NB);
   HistArgs h;
   h.nseg = 1; h.keys = kA; h.seg_stride = n; h.seg_count = meta; h.npass = L.npass; h.pass0 = 0;
   h.bits = L.bits; h.base_shift = 0; h.hist = at<uint32_t>(ws, L.hist);

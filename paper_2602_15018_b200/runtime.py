@@ -105,6 +105,73 @@ class StepEngine:
                                             len(stage_events))
         _lib.check(rc, "evs_step")
 
+    # -- CUDA-graph replay with the device-resident step clock ----------------
+    def capture(self, windows, ref_log, last_event_t, th_pos=None, th_neg=None, tick: int = 1000,
+                t0: int = 0, validate: bool = True):
+        """Capture one CUDA graph running one step per frame window (in order).
+
+        Start times and lookback epochs advance on the device
+        (EVS_FLAG_DEVICE_CLOCK), so ``replay()`` continues the sequence: replay
+        r covers frames [r*len(windows)*T, (r+1)*len(windows)*T) after t0.
+        """
+        import torch
+
+        p = self.params
+        p.flags = _lib.EVS_FLAG_DEVICE_CLOCK
+        p.tick = int(tick)
+        self._graph_steps = len(windows)
+        self._clock_tick = int(tick)
+        self._clock_t0 = int(t0)
+        # (callers run eager steps first so kernel attributes are already set)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(self.graph, stream=s):
+                for win in windows:
+                    self._launch_dc(win, ref_log, last_event_t, th_pos, th_neg, validate)
+        torch.cuda.current_stream().wait_stream(s)
+        p.flags = 0
+        self._graph_args = (ref_log, last_event_t, th_pos, th_neg, windows)
+
+    def _clock_set(self, t0: int, epoch: int):
+        """Point the device clock at (t0, epoch); flags must include DEVICE_CLOCK for sizing."""
+        rc = self.lib.evs_step_clock_init(ctypes.byref(self.params), ctypes.c_void_p(self.workspace.data_ptr()),
+                                          ctypes.c_size_t(self.workspace.numel()), int(t0), int(epoch),
+                                          ctypes.c_void_p(_lib.stream_ptr()))
+        _lib.check(rc, "evs_step_clock_init")
+
+    def _launch_dc(self, frames, ref_log, last_event_t, th_pos, th_neg, validate):
+        p, b = self.params, self.bufs
+        p.validate = 1 if validate else 0
+        b.frames = frames.data_ptr()
+        b.t_bounds = None
+        b.ref_log, b.last_event_t = ref_log.data_ptr(), last_event_t.data_ptr()
+        if self.shape.uniform is None:
+            b.th_pos, b.th_neg = th_pos.data_ptr(), th_neg.data_ptr()
+        else:
+            b.th_pos = b.th_neg = None
+        b.ev_t, b.ev_x = self.ev_t.data_ptr(), self.ev_x.data_ptr()
+        b.ev_y, b.ev_p = self.ev_y.data_ptr(), self.ev_p.data_ptr()
+        b.counts, b.dropped = self.info[0].data_ptr(), self.info[1].data_ptr()
+        b.reservations, b.bad_pixel = self.info[2].data_ptr(), self.bad.data_ptr()
+        rc = self.lib.evs_step(ctypes.byref(p), ctypes.byref(b), ctypes.c_void_p(self.workspace.data_ptr()),
+                               ctypes.c_size_t(self.workspace.numel()), ctypes.c_void_p(_lib.stream_ptr()))
+        _lib.check(rc, "evs_step")
+
+    def replay(self) -> None:
+        """Replay the captured graph on the current stream (no host sync)."""
+        # The graph's steps share the engine's epoch sequence with eager
+        # launches, so stale lookback words can never carry a live epoch.
+        need = self._graph_steps * _lib.EVS_EPOCHS_PER_CALL
+        if self.epochs.value + need > _lib.EVS_EPOCH_LIMIT:
+            self.workspace.zero_()
+            self.epochs.value = 1
+        self._clock_set(self._clock_t0, self.epochs.value)
+        self.graph.replay()
+        self.epochs.value += need
+        self._clock_t0 += self._graph_steps * self.shape.frames * self._clock_tick
+
     def fetch_info(self):
         """Synchronising read of (counts, dropped, reservations, bad)."""
         import torch
