@@ -124,6 +124,11 @@ evs_status evs_canonical_sort(int64_t n, int64_t* t, uint16_t* x, uint16_t* y, i
 evs_status evs_batch_stats(int64_t n, const int64_t* t, const uint16_t* x, const uint16_t* y,
                            const int8_t* p, int64_t* out5, void* stream);
 
+/* Self-test of the kernels' table-driven f64 log (model.py:39 front-end):
+ * out_fast[i] = the log used by evs_step, out_cuda[i] = CUDA's log(x[i]). */
+evs_status evs_selftest_log(int64_t n, const double* x, double* out_fast, double* out_cuda,
+                            void* stream);
+
 /* numpy SeedSequence(seed) -> PCG64 state (host function, no GPU).
  * words: little-endian u32 words of the non-negative seed.
  * out: state_hi, state_lo, inc_hi, inc_lo. */

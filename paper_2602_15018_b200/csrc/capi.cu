@@ -27,7 +27,8 @@ int sm_count_current() {
 }
 
 struct StepLayout {
-  int nseg, ntiles1, npass, bits, NB;
+  int nseg, ntiles1, npass, bits, NB, ngroups;
+  size_t rows, group_base, tot;
   int64_t max_tiles2;
   size_t ctr, desc, status1, hist, gstart, seg_total, seg_tbase, seg_tile_prefix, status2, keysA, keysB,
       total;
@@ -57,12 +58,17 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   L->npass = canon ? (tbits + kMaxDigitBits - 1) / kMaxDigitBits : 0;
   L->bits = canon ? (tbits + L->npass - 1) / L->npass : 0;
   L->NB = canon ? (1 << L->bits) : 0;
-  L->max_tiles2 = canon ? (p->capacity + kOrdTile - 1) / kOrdTile : 0;
+  // generic onesweep passes (k_order) only for t_rel wider than one digit
+  L->max_tiles2 = (canon && L->npass > 1) ? (p->capacity + kOrdTile - 1) / kOrdTile : 0;
+  L->ngroups = (L->ntiles1 + kGroupTiles - 1) / kGroupTiles;
   size_t off = 0;
   L->ctr = off; off = align_up(off + 64 * sizeof(uint32_t));
   L->desc = off; off = align_up(off + sizeof(StepDesc));
   L->status1 = off; off = align_up(off + (size_t)L->nseg * L->ntiles1 * 8);
-  L->hist = off; off = align_up(off + (size_t)L->nseg * L->npass * kHistReps * L->NB * 4);
+  L->rows = off; off = align_up(off + (canon ? (size_t)L->nseg * L->ngroups * L->NB * 4 : 0));
+  L->group_base = off; off = align_up(off + (size_t)L->nseg * L->ngroups * 8);
+  L->tot = off; off = align_up(off + (size_t)L->nseg * L->NB * 4);
+  L->hist = off; off = align_up(off + (L->npass > 1 ? (size_t)L->nseg * L->npass * kHistReps * L->NB * 4 : 0));
   L->gstart = off; off = align_up(off + (size_t)L->nseg * L->NB * 4);
   L->seg_total = off; off = align_up(off + (size_t)L->nseg * 8);
   L->seg_tbase = off; off = align_up(off + (size_t)L->nseg * 8);
@@ -144,7 +150,7 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   g.seg_total = at<int64_t>(ws, L.seg_total);
   g.seg_res = b->reservations;
   g.seg_tbase = at<int64_t>(ws, L.seg_tbase);
-  g.hist = canon ? at<uint32_t>(ws, L.hist) : nullptr;
+  g.hist = nullptr;
   g.npass = L.npass; g.hist_bits = L.bits;
   g.status = at<uint64_t>(ws, L.status1);
   g.tile_ctr = at<uint32_t>(ws, L.ctr);
@@ -152,55 +158,82 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   g.epoch = p->epoch;
   g.ntiles = L.ntiles1;
   g.desc = desc;
+  g.rows = canon ? at<uint32_t>(ws, L.rows) : nullptr;
+  g.group_base = canon ? at<int64_t>(ws, L.group_base) : nullptr;
+  g.ngroups = L.ngroups;
+  g.log_eps_f = (float)p->log_eps;
   e = launch_generate(g, b->th_pos == nullptr, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(2);
 
-  PlanArgs pl;
-  memset(&pl, 0, sizeof(pl));
-  pl.nseg = L.nseg; pl.cap = p->capacity; pl.seg_total = g.seg_total;
-  pl.out_count = b->counts; pl.out_dropped = b->dropped;
-  pl.hist = g.hist; pl.npass = L.npass; pl.pass = 0; pl.bits = L.bits;
-  pl.gstart = at<uint32_t>(ws, L.gstart);
-  pl.seg_tile_prefix = canon ? at<uint32_t>(ws, L.seg_tile_prefix) : nullptr;
-  pl.bad = b->bad_pixel; pl.zero_hist = 1;
-  e = launch_plan(pl, st);
+  if (!canon) {
+    PlanArgs pl;
+    memset(&pl, 0, sizeof(pl));
+    pl.nseg = L.nseg; pl.cap = p->capacity; pl.seg_total = g.seg_total;
+    pl.out_count = b->counts; pl.out_dropped = b->dropped;
+    pl.bad = b->bad_pixel;
+    e = launch_plan(pl, st);
+    if (e != cudaSuccess) return EVS_ERR_CUDA;
+    mark(3);
+    mark(4);
+    return EVS_OK;
+  }
+
+  // pass 0 (lowest t_rel digit): column scan of the K1 group rows + group-CTA ordering
+  ColScanArgs cs;
+  cs.nseg = L.nseg; cs.ngroups = L.ngroups; cs.bits = L.bits; cs.cap = p->capacity;
+  cs.rows = g.rows; cs.tot = at<uint32_t>(ws, L.tot); cs.seg_total = g.seg_total;
+  cs.out_count = b->counts; cs.out_dropped = b->dropped; cs.bad = b->bad_pixel;
+  e = launch_colscan(cs, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(3);
-  if (!canon) { mark(4); return EVS_OK; }
+  GroupOrderArgs go;
+  go.nseg = L.nseg; go.ngroups = L.ngroups; go.bits = L.bits; go.shift = kKeyPixBits;
+  go.keys_in = at<uint64_t>(ws, L.keysA); go.seg_stride = p->capacity;
+  go.rows = g.rows; go.tot = cs.tot; go.group_base = g.group_base; go.seg_count = b->counts;
+  go.final_soa = L.npass == 1; go.keys_out = at<uint64_t>(ws, L.keysB);
+  go.out_t = b->ev_t; go.out_x = b->ev_x; go.out_y = b->ev_y; go.out_p = b->ev_p;
+  go.seg_tbase = g.seg_tbase;
+  e = launch_group_order(go, st);
+  if (e != cudaSuccess) return EVS_ERR_CUDA;
 
   if (L.npass > 1) {
+    // wide t_rel (dt > 2^11 us): remaining digits with generic onesweep passes
     HistArgs h;
-    h.nseg = L.nseg; h.keys = g.keys; h.seg_stride = p->capacity; h.seg_count = b->counts;
-    h.npass = L.npass; h.pass0 = 1; h.bits = L.bits; h.base_shift = kKeyPixBits; h.hist = g.hist;
+    h.nseg = L.nseg; h.keys = go.keys_out; h.seg_stride = p->capacity; h.seg_count = b->counts;
+    h.npass = L.npass; h.pass0 = 1; h.bits = L.bits; h.base_shift = kKeyPixBits;
+    h.hist = at<uint32_t>(ws, L.hist);
     e = launch_hist(h, st);
     if (e != cudaSuccess) return EVS_ERR_CUDA;
-  }
-  const int sms = sm_count_current();
-  for (int pass = 0; pass < L.npass; ++pass) {
-    if (pass > 0) {
-      PlanArgs p2 = pl;
-      p2.out_count = nullptr; p2.out_dropped = nullptr; p2.pass = pass; p2.seg_tile_prefix = nullptr;
-      e = launch_plan(p2, st);
+    const int sms = sm_count_current();
+    for (int pass = 1; pass < L.npass; ++pass) {
+      PlanArgs pl;
+      memset(&pl, 0, sizeof(pl));
+      pl.nseg = L.nseg; pl.cap = p->capacity; pl.seg_total = g.seg_total;
+      pl.hist = h.hist; pl.npass = L.npass; pl.pass = pass; pl.bits = L.bits;
+      pl.gstart = at<uint32_t>(ws, L.gstart);
+      pl.seg_tile_prefix = at<uint32_t>(ws, L.seg_tile_prefix);
+      pl.bad = b->bad_pixel; pl.zero_hist = 1;
+      e = launch_plan(pl, st);
+      if (e != cudaSuccess) return EVS_ERR_CUDA;
+      OrderArgs o;
+      memset(&o, 0, sizeof(o));
+      o.nseg = L.nseg;
+      o.keys_in = (pass % 2 == 1) ? at<uint64_t>(ws, L.keysB) : at<uint64_t>(ws, L.keysA);
+      o.keys_out = (pass % 2 == 1) ? at<uint64_t>(ws, L.keysA) : at<uint64_t>(ws, L.keysB);
+      o.seg_stride = p->capacity; o.seg_count = b->counts;
+      o.seg_tile_prefix = pl.seg_tile_prefix;
+      o.gstart = pl.gstart; o.shift = kKeyPixBits + pass * L.bits; o.bits = L.bits;
+      o.status = at<uint64_t>(ws, L.status2); o.max_tiles = L.max_tiles2;
+      o.ctr = at<uint32_t>(ws, L.ctr) + 1 + pass;
+      o.epoch = dclock ? (uint32_t)(1 + pass) : p->epoch + 1 + pass;
+      o.desc = desc;
+      o.final_soa = pass == L.npass - 1;
+      o.out_t = b->ev_t; o.out_x = b->ev_x; o.out_y = b->ev_y; o.out_p = b->ev_p;
+      o.seg_tbase = g.seg_tbase;
+      e = launch_order(o, sms, st);
       if (e != cudaSuccess) return EVS_ERR_CUDA;
     }
-    OrderArgs o;
-    memset(&o, 0, sizeof(o));
-    o.nseg = L.nseg;
-    o.keys_in = (pass % 2 == 0) ? at<uint64_t>(ws, L.keysA) : at<uint64_t>(ws, L.keysB);
-    o.keys_out = (pass % 2 == 0) ? at<uint64_t>(ws, L.keysB) : at<uint64_t>(ws, L.keysA);
-    o.seg_stride = p->capacity; o.seg_count = b->counts;
-    o.seg_tile_prefix = at<uint32_t>(ws, L.seg_tile_prefix);
-    o.gstart = pl.gstart; o.shift = kKeyPixBits + pass * L.bits; o.bits = L.bits;
-    o.status = at<uint64_t>(ws, L.status2); o.max_tiles = L.max_tiles2;
-    o.ctr = at<uint32_t>(ws, L.ctr) + 1 + pass;
-    o.epoch = dclock ? (uint32_t)(1 + pass) : p->epoch + 1 + pass;
-    o.desc = desc;
-    o.final_soa = pass == L.npass - 1;
-    o.out_t = b->ev_t; o.out_x = b->ev_x; o.out_y = b->ev_y; o.out_p = b->ev_p;
-    o.seg_tbase = g.seg_tbase;
-    e = launch_order(o, sms, st);
-    if (e != cudaSuccess) return EVS_ERR_CUDA;
   }
   mark(4);
   return EVS_OK;
@@ -209,6 +242,12 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
 evs_status evs_step(const evs_step_params* p, const evs_step_buffers* b, void* ws, size_t ws_bytes,
                     void* stream) {
   return step_impl(p, b, ws, ws_bytes, stream, nullptr, 0);
+}
+
+evs_status evs_selftest_log(int64_t n, const double* x, double* out_fast, double* out_cuda, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !out_fast || !out_cuda))) return EVS_ERR_ARG;
+  return launch_selftest_log(x, out_fast, out_cuda, n, static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? EVS_OK : EVS_ERR_CUDA;
 }
 
 evs_status evs_step_clock_init(const evs_step_params* p, void* ws, size_t ws_bytes, int64_t t0,

@@ -87,34 +87,64 @@ __device__ __forceinline__ T block_excl_scan(T v, T* smem, T* total) {
 // Warp-cooperative decoupled lookback (called by a full warp).  `status`
 // points at the tile-status array of one chain; tile `t` has already
 // published its aggregate.  Returns the exclusive prefix for tile t.
+//
+// Wide windows: each round reads kLookWin*32 predecessors at once (lane l,
+// slot m -> tile base - l - 32m), so a whole wave of tiles that publish their
+// aggregates together resolves in one or two L2 round trips instead of
+// walking back 32 tiles per round trip.
+constexpr int kLookWin = 8;
 __device__ __forceinline__ uint64_t warp_lookback(const uint64_t* status, int64_t t, uint32_t epoch) {
   const int lane = threadIdx.x & 31;
   uint64_t excl = 0;
   int64_t base = t - 1;
   while (base >= 0) {
-    int64_t idx = base - lane;
-    uint32_t flag;
-    uint64_t val;
+    uint32_t flag[kLookWin];
+    uint64_t val[kLookWin];
     for (;;) {
-      if (idx >= 0) {
-        uint64_t w = ld_relaxed(status + idx);
-        flag = status_flag(w, epoch);
-        val = status_value(w);
-      } else {
-        flag = (uint32_t)kFlagInc;  // virtual inclusive zero before tile 0
-        val = 0;
+      uint64_t w[kLookWin];
+#pragma unroll
+      for (int m = 0; m < kLookWin; ++m) {
+        const int64_t idx = base - lane - 32 * m;
+        w[m] = idx >= 0 ? ld_relaxed(status + idx) : 0ull;
       }
-      uint32_t inc_mask = __ballot_sync(0xffffffffu, flag == kFlagInc);
-      uint32_t nr_mask = __ballot_sync(0xffffffffu, flag == 0);
-      // lanes 0..first-inclusive (all lanes if none is inclusive yet)
-      uint32_t upto = inc_mask ? ((2u << (__ffs(inc_mask) - 1)) - 1u) : 0xffffffffu;
-      if (nr_mask & upto) continue;  // a needed predecessor is not ready: spin
-      uint64_t mine = ((upto >> lane) & 1u) ? val : 0;
+      // first (nearest) window slot that holds an inclusive prefix
+      int first_m = kLookWin;
+      uint32_t first_mask = 0;
+      bool stall = false;
+#pragma unroll
+      for (int m = 0; m < kLookWin; ++m) {
+        const int64_t idx = base - lane - 32 * m;
+        if (idx >= 0) {
+          flag[m] = status_flag(w[m], epoch);
+          val[m] = status_value(w[m]);
+        } else {
+          flag[m] = (uint32_t)kFlagInc;  // virtual inclusive zero before tile 0
+          val[m] = 0;
+        }
+        const uint32_t inc_mask = __ballot_sync(0xffffffffu, flag[m] == kFlagInc);
+        const uint32_t nr_mask = __ballot_sync(0xffffffffu, flag[m] == 0);
+        if (first_m == kLookWin) {
+          // lanes 0..first-inclusive of this slot (all lanes if none inclusive)
+          const uint32_t upto = inc_mask ? ((2u << (__ffs(inc_mask) - 1)) - 1u) : 0xffffffffu;
+          if (nr_mask & upto) stall = true;
+          if (inc_mask) { first_m = m; first_mask = upto; }
+        }
+      }
+      if (stall) {  // a needed predecessor is not ready: back off, re-read the window
+        __nanosleep(200);
+        continue;
+      }
+      uint64_t mine = 0;
+#pragma unroll
+      for (int m = 0; m < kLookWin; ++m) {
+        if (m < first_m) mine += val[m];
+        else if (m == first_m && ((first_mask >> lane) & 1u)) mine += val[m];
+      }
       excl += warp_sum(mine);
-      if (inc_mask) return excl;
+      if (first_m < kLookWin) return excl;
       break;
     }
-    base -= 32;
+    base -= 32 * kLookWin;
   }
   return excl;
 }

@@ -57,6 +57,43 @@ struct GenArgs {
   uint32_t epoch;
   int ntiles;  // tiles per stream frame
   const StepDesc* desc;  // non-null: t0 / epoch come from the device clock
+  // per tile-group t_rel histogram rows (canonical order, pass 0):
+  // rows[seg][group][NB], group = tile / kGroupTiles; group_base[seg][group]
+  uint32_t* rows;
+  int64_t* group_base;
+  int ngroups;
+  float log_eps_f;  // log_eps rounded to f32 (prefilter only)
+  double rth_pos, rth_neg;  // 1/th for uniform thresholds (set by launch_generate)
+};
+
+constexpr int kGroupTiles = 4;  // K1 tiles per histogram row / per K2 CTA
+
+struct ColScanArgs {
+  int nseg, ngroups, bits;
+  int64_t cap;
+  uint32_t* rows;             // in: counts, out: exclusive prefix over groups
+  uint32_t* tot;              // out [nseg][NB]
+  const int64_t* seg_total;
+  int64_t* out_count;
+  int64_t* out_dropped;
+  const int64_t* bad;
+};
+
+struct GroupOrderArgs {
+  int nseg, ngroups, bits, shift;
+  const uint64_t* keys_in;
+  int64_t seg_stride;
+  uint32_t* rows;             // exclusive group prefixes (zeroed after use)
+  const uint32_t* tot;        // [nseg][NB]
+  const int64_t* group_base;  // [nseg][ngroups]
+  const int64_t* seg_count;   // written events per segment
+  int final_soa;
+  uint64_t* keys_out;
+  int64_t* out_t;
+  uint16_t* out_x;
+  uint16_t* out_y;
+  int8_t* out_p;
+  const int64_t* seg_tbase;
 };
 
 struct PlanArgs {
@@ -113,5 +150,9 @@ cudaError_t launch_generate(const GenArgs& a, int uniform_th, cudaStream_t st);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t st);
 cudaError_t launch_hist(const HistArgs& a, cudaStream_t st);
 cudaError_t launch_order(const OrderArgs& a, int sm_count, cudaStream_t st);
+cudaError_t launch_colscan(const ColScanArgs& a, cudaStream_t st);
+cudaError_t launch_selftest_log(const double* x, double* out_fast, double* out_ref, int64_t n,
+                                cudaStream_t st);
+cudaError_t launch_group_order(const GroupOrderArgs& a, cudaStream_t st);
 
 }  // namespace evs

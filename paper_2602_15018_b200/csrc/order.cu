@@ -2,12 +2,7 @@
 //
 //   k_prologue  : frame validation (reference ValueError semantics,
 //                 model.py:28-39) + per-call accumulator reset.
-//   k_generate  : K1 -- fused log / threshold / crossing count / refractory /
-//                 state update, warp-ballot chunk stats, block scan +
-//                 decoupled-lookback placement of the variable-length
-//                 per-pixel output in pixel-major (serial) order
-//                 (model.py:79-171 == parallel.py:126-273), smem-staged
-//                 coalesced writes, per-tile t_rel histogram.
+//   (k_generate, the fused K1, lives in generate.cu)
 //   k_plan      : per-segment counts / capacity (parallel.py:261-273),
 //                 histogram reduction + bin starts, work list for k_order.
 //   k_hist      : digit histograms of a key array (generic sort passes).
@@ -88,246 +83,6 @@ cudaError_t launch_prologue(const float* frames, int64_t nframes_px, int64_t P, 
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------
-// K1: fused generate
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int64_t t_rel_of(int j, double thd, double adiff, double dtd, int64_t dt) {
-  // model.py:144-146: int(((j*th)/|diff|)*dt), clamped to dt-1
-  int64_t tr = (int64_t)((((double)j * thd) / adiff) * dtd);
-  return tr > dt - 1 ? dt - 1 : tr;
-}
-
-template <int MODE>
-__device__ __forceinline__ void put_event(const GenArgs& a, int64_t segoff, int64_t g, uint64_t key,
-                                          int64_t tprev) {
-  if (MODE == 0) {
-    a.out_t[segoff + g] = tprev + (int64_t)(key >> kKeyPixBits);
-    a.out_x[segoff + g] = (uint16_t)((key >> 1) & 0xffffu);
-    a.out_y[segoff + g] = (uint16_t)((key >> 17) & 0xffffu);
-    a.out_p[segoff + g] = (key & 1u) ? (int8_t)1 : (int8_t)-1;
-  } else {
-    a.keys[segoff + g] = key;
-  }
-}
-
-template <bool VEC, bool REFR, bool UNI, int MODE>
-__global__ void __launch_bounds__(kGenThreads, 3) k_generate(GenArgs a) {
-  constexpr int NT = kGenThreads, VPT = kGenVpt, TILE = kGenTile, NW = NT / 32;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t* stg = reinterpret_cast<uint64_t*>(smem_raw);  // [kGenStage]
-  uint32_t* hs = reinterpret_cast<uint32_t*>(stg + kGenStage);
-  __shared__ int64_t s_scan[NW + 1];
-  __shared__ uint32_t s_id;
-  __shared__ int64_t s_base;
-  __shared__ int s_res;
-
-  const int tid = threadIdx.x, lane = tid & 31;
-  if (tid == 0) {
-    uint32_t id = atomicAdd(a.tile_ctr, 1u);
-    if (id == gridDim.x - 1) atomicExch(a.tile_ctr, 0u);  // last fetch: reset for next launch
-    s_id = id;
-    s_res = 0;
-  }
-  const int NB = a.hist ? (1 << a.hist_bits) : 0;
-  for (int d = tid; d < NB; d += NT) hs[d] = 0;
-  __syncthreads();
-  if (*a.bad != kNoBad) return;  // validation failed: state is not touched
-
-  const uint32_t id = s_id;
-  const int s = (int)(id / (uint32_t)a.ntiles);
-  const int tile = (int)(id % (uint32_t)a.ntiles);
-  const int64_t P = a.P;
-  const uint32_t epoch = a.desc ? a.desc->cur_epoch : a.epoch;
-  const int64_t clock_t0 = a.desc ? a.desc->cur_t0 : a.t0;
-  const int64_t pix0 = (int64_t)tile * TILE + (int64_t)tid * VPT;
-  const bool full = VEC && (pix0 + VPT <= P);
-  float* refp = a.ref + (int64_t)s * P;
-  int64_t* lastp = a.last + (int64_t)s * P;
-
-  float r[VPT], thp[VPT], thn[VPT];
-  int64_t lt[VPT];
-  bool dirty[VPT];
-#pragma unroll
-  for (int k = 0; k < VPT; ++k) { r[k] = 0.f; lt[k] = 0; dirty[k] = false; thp[k] = a.thp_u; thn[k] = a.thn_u; }
-  if (full) {
-    float4 q = *reinterpret_cast<const float4*>(refp + pix0);
-    r[0] = q.x; r[1] = q.y; r[2] = q.z; r[3] = q.w;
-    if (REFR) {
-      longlong2 l0 = *reinterpret_cast<const longlong2*>(lastp + pix0);
-      longlong2 l1 = *reinterpret_cast<const longlong2*>(lastp + pix0 + 2);
-      lt[0] = l0.x; lt[1] = l0.y; lt[2] = l1.x; lt[3] = l1.y;
-    }
-    if (!UNI) {
-      float4 p4 = *reinterpret_cast<const float4*>(a.thp + (int64_t)s * P + pix0);
-      float4 n4 = *reinterpret_cast<const float4*>(a.thn + (int64_t)s * P + pix0);
-      thp[0] = p4.x; thp[1] = p4.y; thp[2] = p4.z; thp[3] = p4.w;
-      thn[0] = n4.x; thn[1] = n4.y; thn[2] = n4.z; thn[3] = n4.w;
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      if (pix0 + k < P) {
-        r[k] = refp[pix0 + k];
-        if (REFR) lt[k] = lastp[pix0 + k];
-        if (!UNI) { thp[k] = a.thp[(int64_t)s * P + pix0 + k]; thn[k] = a.thn[(int64_t)s * P + pix0 + k]; }
-      }
-    }
-  }
-
-  for (int f = 0; f < a.T; ++f) {
-    const int seg = s * a.T + f;
-    int64_t tprev, tnow;
-    if (a.t_bounds) {
-      tprev = a.t_bounds[(int64_t)s * (a.T + 1) + f];
-      tnow = a.t_bounds[(int64_t)s * (a.T + 1) + f + 1];
-    } else {
-      tprev = clock_t0 + (int64_t)f * a.tick;
-      tnow = tprev + a.tick;
-    }
-    const int64_t dt = tnow - tprev;
-    const double dtd = (double)dt;
-    const float* fr = a.frames + ((int64_t)s * a.T + f) * P;
-    float v[VPT];
-    if (full) {
-      float4 q = __ldcs(reinterpret_cast<const float4*>(fr + pix0));
-      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-    } else {
-#pragma unroll
-      for (int k = 0; k < VPT; ++k) v[k] = (pix0 + k < P) ? __ldcs(fr + pix0 + k) : 0.f;
-    }
-
-    // ---- lane math, count pass (model.py:124-163) ----
-    double adiff[VPT];
-    float thv[VPT];
-    int nn[VPT], kept[VPT];
-    int64_t last0[VPT];
-    int tot = 0;
-#pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      nn[k] = 0; kept[k] = 0; adiff[k] = 0.0; thv[k] = 1.f; last0[k] = lt[k];
-      if (pix0 + k < P) {
-        const double ln = log((double)v[k] + a.log_eps);  // model.py:39 (f64)
-        const double ls = (double)r[k];
-        const double diff = ln - ls;
-        if (diff != 0.0) {
-          const bool pos = diff > 0.0;
-          const float th = pos ? thp[k] : thn[k];
-          const double thd = (double)th;
-          const double ad = pos ? diff : -diff;
-          double q = ad / thd + 1e-4;  // model.py:137
-          int n = q >= 2147483647.0 ? 2147483647 : (int)q;
-          if (n > 0) {
-            adiff[k] = ad; thv[k] = pos ? th : -th; nn[k] = n;
-            int kc;
-            if (REFR) {
-              int64_t l = lt[k];
-              kc = 0;
-              for (int j = 1; j <= n; ++j) {
-                int64_t t = tprev + t_rel_of(j, thd, ad, dtd, dt);
-                if (t - l < a.refr) continue;  // model.py:148-149
-                l = t;
-                ++kc;
-              }
-              lt[k] = l;
-            } else {
-              kc = n;
-              lt[k] = tprev + t_rel_of(n, thd, ad, dtd, dt);
-            }
-            kept[k] = kc;
-            const double step = (double)n * thd;  // exact in f64
-            r[k] = (float)(pos ? ls + step : ls - step);  // model.py:159-162
-            dirty[k] = true;
-            tot += kc;
-          }
-        }
-      }
-    }
-
-    // ---- chunk reservations (warp ballot; 8 lanes = one 32-pixel chunk) ----
-    {
-      uint32_t m = __ballot_sync(0xffffffffu, tot > 0);
-      if (lane == 0) {
-        int c = ((m & 0xffu) != 0) + ((m & 0xff00u) != 0) + ((m & 0xff0000u) != 0) + ((m & 0xff000000u) != 0);
-        if (c) atomicAdd(&s_res, c);
-      }
-    }
-
-    // ---- block scan + decoupled lookback ----
-    int64_t tile_total;
-    const int64_t excl = block_excl_scan<NT, int64_t>((int64_t)tot, s_scan, &tile_total);
-    if (tid < 32) {
-      uint64_t* st = a.status + (int64_t)seg * a.ntiles;
-      uint64_t ex = 0;
-      if (tile == 0) {
-        if (lane == 0) st_relaxed(st, pack_status(kFlagInc, epoch, (uint64_t)tile_total));
-      } else {
-        if (lane == 0) st_relaxed(st + tile, pack_status(kFlagAgg, epoch, (uint64_t)tile_total));
-        ex = warp_lookback(st, tile, epoch);
-        if (lane == 0) st_relaxed(st + tile, pack_status(kFlagInc, epoch, ex + (uint64_t)tile_total));
-      }
-      if (lane == 0) {
-        s_base = (int64_t)ex;
-        if (tile == a.ntiles - 1) a.seg_total[seg] = (int64_t)ex + tile_total;
-        if (tile == 0) a.seg_tbase[seg] = tprev;
-      }
-    }
-    __syncthreads();
-    const int64_t base = s_base;
-    int64_t nstore = a.cap - base;
-    nstore = nstore < 0 ? 0 : (nstore > tile_total ? tile_total : nstore);
-    const bool staged = nstore <= kGenStage;
-    const int64_t segoff = (int64_t)seg * a.seg_stride;
-
-    // ---- emission (pixel-major, chronological within a pixel) ----
-    int64_t o = excl;
-#pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      if (kept[k] > 0 && o < nstore) {
-        const int64_t pix = pix0 + k;
-        const uint64_t xy = ((uint64_t)(pix / a.W) << 17) | ((uint64_t)(pix % a.W) << 1) | (thv[k] > 0.f ? 1u : 0u);
-        const double thd = (double)fabsf(thv[k]);
-        int64_t l = last0[k];
-        for (int j = 1; j <= nn[k] && o < nstore; ++j) {
-          const int64_t tr = t_rel_of(j, thd, adiff[k], dtd, dt);
-          if (REFR) {
-            if (tprev + tr - l < a.refr) continue;
-            l = tprev + tr;
-          }
-          const uint64_t key = ((uint64_t)tr << kKeyPixBits) | xy;
-          if (staged) stg[o] = key;
-          else put_event<MODE>(a, segoff, base + o, key, tprev);
-          if (NB) atomicAdd(&hs[(uint32_t)tr & (uint32_t)(NB - 1)], 1u);
-          ++o;
-        }
-      }
-    }
-    __syncthreads();
-    if (staged) {
-      for (int64_t i = tid; i < nstore; i += NT) put_event<MODE>(a, segoff, base + i, stg[i], tprev);
-    }
-    if (NB) {
-      uint32_t* hg = a.hist + (((int64_t)seg * a.npass + 0) * kHistReps + (tile % kHistReps)) * NB;
-      for (int d = tid; d < NB; d += NT) {
-        uint32_t c = hs[d];
-        if (c) { atomicAdd(hg + d, c); hs[d] = 0; }
-      }
-    }
-    if (tid == 0 && s_res) { atomicAdd(reinterpret_cast<unsigned long long*>(a.seg_res + seg), (unsigned long long)s_res); s_res = 0; }
-    __syncthreads();
-  }
-
-  // ---- state write-back (only pixels that crossed a threshold) ----
-  if (full && dirty[0] && dirty[1] && dirty[2] && dirty[3]) {
-    *reinterpret_cast<float4*>(refp + pix0) = make_float4(r[0], r[1], r[2], r[3]);
-    *reinterpret_cast<longlong2*>(lastp + pix0) = make_longlong2(lt[0], lt[1]);
-    *reinterpret_cast<longlong2*>(lastp + pix0 + 2) = make_longlong2(lt[2], lt[3]);
-  } else {
-#pragma unroll
-    for (int k = 0; k < VPT; ++k)
-      if (dirty[k]) { refp[pix0 + k] = r[k]; lastp[pix0 + k] = lt[k]; }
-  }
-}
-
 // Raise a kernel's dynamic-smem limit once per process (not per launch).
 template <typename K>
 static void ensure_smem(K k, size_t smem) {
@@ -341,34 +96,6 @@ static void ensure_smem(K k, size_t smem) {
   if (ndone < 64) done[ndone++] = key;
 }
 
-template <bool VEC, bool REFR, bool UNI>
-static cudaError_t gen_dispatch_mode(const GenArgs& a, unsigned grid, size_t smem, cudaStream_t st) {
-  if (a.mode == 0) {
-    auto k = k_generate<VEC, REFR, UNI, 0>;
-    ensure_smem(k, smem);
-    k<<<grid, kGenThreads, smem, st>>>(a);
-  } else {
-    auto k = k_generate<VEC, REFR, UNI, 1>;
-    ensure_smem(k, smem);
-    k<<<grid, kGenThreads, smem, st>>>(a);
-  }
-  return cudaGetLastError();
-}
-
-cudaError_t launch_generate(const GenArgs& a, int uniform_th, cudaStream_t st) {
-  const unsigned grid = (unsigned)((int64_t)a.S * a.ntiles);
-  const int NB = a.hist ? (1 << a.hist_bits) : 0;
-  const size_t smem = (size_t)kGenStage * 8 + (size_t)NB * 4;
-  bool vec = (a.P % 4 == 0) && ((uintptr_t)a.frames % 16 == 0) && ((uintptr_t)a.ref % 16 == 0) &&
-             ((uintptr_t)a.last % 16 == 0) && (uniform_th || (((uintptr_t)a.thp % 16 == 0) && ((uintptr_t)a.thn % 16 == 0)));
-  bool refr = a.refr > 0;
-  if (vec) {
-    if (refr) return uniform_th ? gen_dispatch_mode<true, true, true>(a, grid, smem, st) : gen_dispatch_mode<true, true, false>(a, grid, smem, st);
-    return uniform_th ? gen_dispatch_mode<true, false, true>(a, grid, smem, st) : gen_dispatch_mode<true, false, false>(a, grid, smem, st);
-  }
-  if (refr) return uniform_th ? gen_dispatch_mode<false, true, true>(a, grid, smem, st) : gen_dispatch_mode<false, true, false>(a, grid, smem, st);
-  return uniform_th ? gen_dispatch_mode<false, false, true>(a, grid, smem, st) : gen_dispatch_mode<false, false, false>(a, grid, smem, st);
-}
 
 // ---------------------------------------------------------------------------
 // plan: counts, bin starts, work list
@@ -594,7 +321,7 @@ __global__ void __launch_bounds__(kOrdThreads) k_order(OrderArgs a) {
             const int d = tid + j * NT;
             if (d < NB && jj[j] >= 0) {
               const uint32_t fl = status_flag(wv[j], epoch);
-              if (fl == 0) { pending = true; continue; }
+              if (fl == 0) { pending = true; __nanosleep(100); continue; }
               ex[j] += status_value(wv[j]);
               jj[j] = (fl == kFlagInc) ? -1 : jj[j] - 1;
               if (jj[j] >= 0) pending = true;
@@ -658,6 +385,205 @@ cudaError_t launch_order(const OrderArgs& a, int sm_count, cudaStream_t st) {
     occ_cache[a.bits] = per_sm;
   }
   k_order<<<sm_count * per_sm, kOrdThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// column scan: per (segment, bin) exclusive prefix of the tile-group
+// histogram rows over groups (pixel order) + bin totals; counts/capacity.
+// ---------------------------------------------------------------------------
+// Block = 32 bins x 16 group-chunks: every thread issues its chunk's loads
+// at once (one L2 round trip), then chunk sums are scanned in smem.
+constexpr int kCsBins = 32, kCsChunks = 16;
+__global__ void __launch_bounds__(kCsBins * kCsChunks) k_colscan(ColScanArgs a) {
+  __shared__ uint32_t s_sum[kCsChunks][kCsBins];
+  const int NB = 1 << a.bits;
+  const int seg = blockIdx.y;
+  const int bl = threadIdx.x % kCsBins, ch = threadIdx.x / kCsBins;
+  const int d = blockIdx.x * kCsBins + bl;
+  const bool bad = *a.bad != kNoBad;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.out_count) {
+    const int64_t total = bad ? 0 : a.seg_total[seg];
+    const int64_t w = total < a.cap ? total : a.cap;
+    a.out_count[seg] = w;
+    a.out_dropped[seg] = total - w;
+  }
+  const int CH = (a.ngroups + kCsChunks - 1) / kCsChunks;
+  const int g0 = ch * CH, g1 = min(a.ngroups, g0 + CH);
+  uint32_t* col = a.rows + (int64_t)seg * a.ngroups * NB + d;
+  constexpr int kMaxCh = 32;
+  uint32_t c[kMaxCh];
+  uint32_t sum = 0;
+  if (d < NB) {
+#pragma unroll
+    for (int u = 0; u < kMaxCh; ++u) c[u] = (g0 + u < g1) ? col[(int64_t)(g0 + u) * NB] : 0u;
+    // (groups beyond kMaxCh per chunk are handled by the tail loop below)
+#pragma unroll
+    for (int u = 0; u < kMaxCh; ++u) sum += c[u];
+    for (int g = g0 + kMaxCh; g < g1; ++g) sum += col[(int64_t)g * NB];
+  }
+  s_sum[ch][bl] = sum;
+  __syncthreads();
+  uint32_t acc = 0, tot = 0;
+  for (int k = 0; k < kCsChunks; ++k) {
+    const uint32_t v = s_sum[k][bl];
+    if (k < ch) acc += v;
+    tot += v;
+  }
+  if (d < NB) {
+#pragma unroll
+    for (int u = 0; u < kMaxCh; ++u)
+      if (g0 + u < g1) { col[(int64_t)(g0 + u) * NB] = acc; acc += c[u]; }
+    for (int g = g0 + kMaxCh; g < g1; ++g) {
+      const uint32_t v = col[(int64_t)g * NB];
+      col[(int64_t)g * NB] = acc;
+      acc += v;
+    }
+    if (ch == 0) a.tot[(int64_t)seg * NB + d] = bad ? 0u : tot;
+  }
+}
+
+cudaError_t launch_colscan(const ColScanArgs& a, cudaStream_t st) {
+  const int NB = 1 << a.bits;
+  dim3 grid((NB + kCsBins - 1) / kCsBins, a.nseg);
+  k_colscan<<<grid, kCsBins * kCsChunks, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K2 (group form): one CTA per (segment, tile group).  The group's keys are
+// already in pixel order; a stable counting pass by t_rel places them at
+// bin start + prefix of earlier groups (column scan) + running sub-tile
+// offset + warp match-any rank.  No inter-CTA waiting.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kOrdThreads) k_group_order(GroupOrderArgs a) {
+  constexpr int NT = kOrdThreads, IPT = kOrdIpt, M = kOrdTile, NW = NT / 32;
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int NB = 1 << a.bits;
+  uint64_t* sorted = reinterpret_cast<uint64_t*>(sm);
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(sorted + M);  // [NW][NB]
+  uint32_t* lstart = reinterpret_cast<uint32_t*>(wcnt + NW * NB);
+  uint32_t* offr = lstart + NB;
+  uint32_t* stot = offr + NB;
+  __shared__ uint32_t s_scan[NW + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int seg = blockIdx.y, g = blockIdx.x;
+  const uint64_t dmask = (uint64_t)(NB - 1);
+  const int per = (NB + NT - 1) / NT;
+
+  const int64_t n = a.seg_count[seg];
+  int64_t lo = a.group_base[(int64_t)seg * a.ngroups + g];
+  int64_t hi = (g + 1 < a.ngroups) ? a.group_base[(int64_t)seg * a.ngroups + g + 1] : n;
+  lo = lo < n ? lo : n;
+  hi = hi < n ? hi : n;
+  if (n == 0) lo = hi = 0;
+
+  // running global offset per bin: bin start (scan of totals) + earlier groups
+  uint32_t* row = a.rows + ((int64_t)seg * a.ngroups + g) * NB;
+  {
+    uint32_t sum = 0;
+    for (int j = 0; j < per; ++j) { const int d = tid * per + j; if (d < NB) sum += a.tot[(int64_t)seg * NB + d]; }
+    uint32_t tt;
+    uint32_t ex = block_excl_scan<NT, uint32_t>(sum, s_scan, &tt);
+    for (int j = 0; j < per; ++j) {
+      const int d = tid * per + j;
+      if (d < NB) {
+        offr[d] = ex + row[d];
+        row[d] = 0;  // rows are accumulated with atomics by the next step's K1
+        ex += a.tot[(int64_t)seg * NB + d];
+      }
+    }
+  }
+  __syncthreads();
+  const uint64_t* kin = a.keys_in + (int64_t)seg * a.seg_stride;
+  const int64_t ob = (int64_t)seg * a.seg_stride;
+  const int64_t tb0 = a.seg_tbase ? a.seg_tbase[seg] : 0;
+
+  for (int64_t base = lo; base < hi; base += M) {
+    const int cnt = (int)((hi - base) < M ? (hi - base) : M);
+    for (int d = lane; d < NB; d += 32) wcnt[warp * NB + d] = 0;
+    __syncwarp();
+    uint64_t key[IPT];
+    uint32_t rank[IPT];
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      const int idx = warp * 32 * IPT + k * 32 + lane;
+      key[k] = idx < cnt ? __ldcs(kin + base + idx) : 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      const int idx = warp * 32 * IPT + k * 32 + lane;
+      const bool valid = idx < cnt;
+      const int d = valid ? (int)((key[k] >> a.shift) & dmask) : NB;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const int leader = __ffs(peers) - 1;
+      uint32_t old = 0;
+      if (valid && lane == leader) {
+        old = wcnt[warp * NB + d];
+        wcnt[warp * NB + d] = (uint16_t)(old + __popc(peers));
+      }
+      old = __shfl_sync(0xffffffffu, old, leader);
+      rank[k] = old + __popc(peers & lanemask_lt());
+      __syncwarp();
+    }
+    __syncthreads();
+    for (int d = tid; d < NB; d += NT) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int w2 = 0; w2 < NW; ++w2) {
+        const uint32_t c = wcnt[w2 * NB + d];
+        wcnt[w2 * NB + d] = (uint16_t)acc;
+        acc += c;
+      }
+      stot[d] = acc;
+    }
+    __syncthreads();
+    {
+      uint32_t sum = 0;
+      for (int j = 0; j < per; ++j) { const int d = tid * per + j; if (d < NB) sum += stot[d]; }
+      uint32_t tt;
+      uint32_t ex = block_excl_scan<NT, uint32_t>(sum, s_scan, &tt);
+      for (int j = 0; j < per; ++j) { const int d = tid * per + j; if (d < NB) { lstart[d] = ex; ex += stot[d]; } }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      const int idx = warp * 32 * IPT + k * 32 + lane;
+      if (idx < cnt) {
+        const int d = (int)((key[k] >> a.shift) & dmask);
+        sorted[lstart[d] + wcnt[warp * NB + d] + rank[k]] = key[k];
+      }
+    }
+    __syncthreads();
+    if (a.final_soa) {
+      for (int i = tid; i < cnt; i += NT) {
+        const uint64_t k = sorted[i];
+        const int d = (int)((k >> a.shift) & dmask);
+        const int64_t gp = ob + (int64_t)(offr[d] + (uint32_t)i - lstart[d]);
+        a.out_t[gp] = tb0 + (int64_t)(k >> kKeyPixBits);
+        a.out_x[gp] = (uint16_t)((k >> 1) & 0xffffu);
+        a.out_y[gp] = (uint16_t)((k >> 17) & 0xffffu);
+        a.out_p[gp] = (k & 1u) ? (int8_t)1 : (int8_t)-1;
+      }
+    } else {
+      for (int i = tid; i < cnt; i += NT) {
+        const uint64_t k = sorted[i];
+        const int d = (int)((k >> a.shift) & dmask);
+        a.keys_out[ob + (int64_t)(offr[d] + (uint32_t)i - lstart[d])] = k;
+      }
+    }
+    __syncthreads();
+    for (int d = tid; d < NB; d += NT) offr[d] += stot[d];
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_group_order(const GroupOrderArgs& a, cudaStream_t st) {
+  const int NB = 1 << a.bits;
+  const size_t smem = (size_t)kOrdTile * 8 + (size_t)(kOrdThreads / 32) * NB * 2 + (size_t)NB * 12;
+  ensure_smem(k_group_order, smem);
+  dim3 grid(a.ngroups, a.nseg);
+  k_group_order<<<grid, kOrdThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
