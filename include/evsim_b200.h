@@ -124,6 +124,57 @@ evs_status evs_canonical_sort(int64_t n, int64_t* t, uint16_t* x, uint16_t* y, i
 evs_status evs_batch_stats(int64_t n, const int64_t* t, const uint16_t* x, const uint16_t* y,
                            const int8_t* p, int64_t* out5, void* stream);
 
+/* Background noise (inject_noise_events, model.py:174-212), bit-exact with
+ * numpy's Generator(PCG64(SeedSequence(seed))) draw order.  The caller
+ * computes lam = rate * (dt * 1e-6) and enlam = exp(-lam) on the host (as
+ * numpy does) and the PCG64 state with evs_seed_pcg64. */
+typedef struct evs_noise_params {
+  int32_t width, height;
+  int64_t t_prev, t_now;
+  double lam;         /* > 0 */
+  double enlam;       /* exp(-lam) */
+  uint64_t pcg[4];    /* state_hi, state_lo, inc_hi, inc_lo */
+  int64_t capacity;   /* event capacity; 0 = automatic (mean + 12 sigma) */
+  int32_t order;      /* 0: reference order -> ev_t/x/y/p; 1: (pixel, p, t) keys -> ev_key */
+  uint32_t reserved;
+  double draw_scale;  /* >= 1; enlarge the walked draw range (retry when meta[2] != 0) */
+} evs_noise_params;
+size_t evs_noise_workspace_bytes(const evs_noise_params* p);
+/* capacity the call will use (host) */
+int64_t evs_noise_capacity(const evs_noise_params* p);
+/* meta_out (device, 4 x int64): [0] draws consumed by the counts, [1] events,
+ * [2] != 0: draw range too short (retry with larger draw_scale),
+ * [3] != 0: events exceed capacity (retry with larger capacity). */
+evs_status evs_noise(const evs_noise_params* p, int64_t* ev_t, uint16_t* ev_x, uint16_t* ev_y,
+                     int8_t* ev_p, uint64_t* ev_key, int64_t* meta_out, void* workspace,
+                     size_t workspace_bytes, void* stream);
+
+/* accumulate_events_to_image (model.py:249-262) of a device batch into an
+ * int64 (H, W) grid; the caller checks coordinate bounds first (ValueError,
+ * model.py:253-254, see evs_batch_stats). */
+evs_status evs_accumulate(int64_t n, const int64_t* t, const uint16_t* x, const uint16_t* y,
+                          const int8_t* p, int64_t window_us, int64_t t_end, int32_t width,
+                          int32_t height, int64_t* grid, void* stream);
+
+/* Voxel grid (no reference counterpart): out[b][y][x]
+ * = sum over events with t in [t0, t1) of p * max(0, D - |b*D - (B-1)(t-t0)|) / D,
+ * D = t1 - t0, accumulated exactly in int64, rounded once to f32. */
+size_t evs_voxel_workspace_bytes(int32_t bins, int32_t width, int32_t height);
+evs_status evs_voxel(int64_t n, const int64_t* t, const uint16_t* x, const uint16_t* y,
+                     const int8_t* p, int64_t t0, int64_t t1, int32_t bins, int32_t width,
+                     int32_t height, float* out, void* workspace, size_t workspace_bytes,
+                     void* stream);
+
+/* limit_bandwidth (model.py:215-246) of a t-sorted device batch of n >= 1
+ * events: keeps the first `cap` = int(rate * window * 1e-6) events of each
+ * window tiling forward from t[0].  meta_out (device, 2 x int64): [0] kept
+ * count, [1] != 0 if the batch is not t-sorted (reference ValueError). */
+size_t evs_limit_bandwidth_workspace_bytes(int64_t n);
+evs_status evs_limit_bandwidth(int64_t n, const int64_t* t, const uint16_t* x, const uint16_t* y,
+                               const int8_t* p, int64_t cap, int64_t window_us, int64_t* out_t,
+                               uint16_t* out_x, uint16_t* out_y, int8_t* out_p, int64_t* meta_out,
+                               void* workspace, size_t workspace_bytes, void* stream);
+
 /* Self-test of the kernels' table-driven f64 log (model.py:39 front-end):
  * out_fast[i] = the log used by evs_step, out_cuda[i] = CUDA's log(x[i]). */
 evs_status evs_selftest_log(int64_t n, const double* x, double* out_fast, double* out_cuda,

@@ -62,7 +62,8 @@ class NoiseParams(ctypes.Structure):
         ("t_prev", ctypes.c_int64), ("t_now", ctypes.c_int64),
         ("lam", ctypes.c_double), ("enlam", ctypes.c_double),
         ("pcg", ctypes.c_uint64 * 4),
-        ("capacity", ctypes.c_int64), ("order", ctypes.c_int32), ("epoch", ctypes.c_uint32),
+        ("capacity", ctypes.c_int64), ("order", ctypes.c_int32), ("reserved", ctypes.c_uint32),
+        ("draw_scale", ctypes.c_double),
     ]
 
 
@@ -116,17 +117,19 @@ def _bind_extras(L) -> None:
     i64 = ctypes.c_int64
     i32 = ctypes.c_int32
     sz = ctypes.c_size_t
-    if hasattr(L, "evs_noise"):
-        L.evs_noise_workspace_bytes.restype = sz
-        L.evs_noise_workspace_bytes.argtypes = [ctypes.POINTER(NoiseParams)]
-        L.evs_noise.argtypes = [ctypes.POINTER(NoiseParams), P, P, P, P, P, P, sz, P]
-    if hasattr(L, "evs_accumulate"):
-        L.evs_accumulate.argtypes = [i64, P, P, P, P, i64, i64, i32, i32, P, P]
-        L.evs_voxel.argtypes = [i64, P, P, P, P, i64, i64, i32, i32, i32, P, P, sz, P]
-        L.evs_limit_bandwidth_workspace_bytes.restype = sz
-        L.evs_limit_bandwidth_workspace_bytes.argtypes = [i64]
-        L.evs_limit_bandwidth.argtypes = [i64, P, P, P, P, ctypes.c_double, i64, P, P, P, P, P,
-                                          P, sz, P]
+    L.evs_noise_workspace_bytes.restype = sz
+    L.evs_noise_workspace_bytes.argtypes = [ctypes.POINTER(NoiseParams)]
+    L.evs_noise_capacity.restype = i64
+    L.evs_noise_capacity.argtypes = [ctypes.POINTER(NoiseParams)]
+    L.evs_noise.argtypes = [ctypes.POINTER(NoiseParams), P, P, P, P, P, P, P, sz, P]
+    L.evs_accumulate.argtypes = [i64, P, P, P, P, i64, i64, i32, i32, P, P]
+    L.evs_voxel_workspace_bytes.restype = sz
+    L.evs_voxel_workspace_bytes.argtypes = [i32, i32, i32]
+    L.evs_voxel.argtypes = [i64, P, P, P, P, i64, i64, i32, i32, i32, P, P, sz, P]
+    L.evs_limit_bandwidth_workspace_bytes.restype = sz
+    L.evs_limit_bandwidth_workspace_bytes.argtypes = [i64]
+    L.evs_limit_bandwidth.argtypes = [i64, P, P, P, P, i64, i64, P, P, P, P, P, P, sz, P]
+    L.evs_selftest_log.argtypes = [i64, P, P, P, P]
 
 
 def check(rc: int, what: str) -> None:

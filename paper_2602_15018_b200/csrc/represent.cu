@@ -1,0 +1,193 @@
+// Event representations and post-processing on device batches.
+//
+//   evs_accumulate      accumulate_events_to_image (model.py:249-262): signed
+//                       polarity sum per pixel over t in [t_end - w, t_end).
+//   evs_voxel           repo-defined 5-bin (B-bin) voxel grid: exact integer
+//                       bilinear-in-time weights, one f32 rounding at the end.
+//   evs_limit_bandwidth limit_bandwidth (model.py:215-246): keep the first
+//                       floor(rate * window) events of every window that
+//                       tiles forward from the first event.
+// The simulator path fuses the histogram / voxel accumulation into the
+// generate kernel (each lane owns its pixels, no atomics); these entry points
+// serve arbitrary batches and the noise events.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/evsim_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace evs {
+
+__global__ void __launch_bounds__(256) k_accumulate(int64_t n, const int64_t* __restrict__ t,
+                                                    const uint16_t* __restrict__ x,
+                                                    const uint16_t* __restrict__ y,
+                                                    const int8_t* __restrict__ p, int64_t lo, int64_t hi,
+                                                    int32_t W, unsigned long long* grid) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ti = t[i];
+    if (ti >= lo && ti < hi)  // model.py:259
+      atomicAdd(grid + (int64_t)y[i] * W + x[i], (unsigned long long)(int64_t)p[i]);
+  }
+}
+
+// voxel numerators: acc[b][pix] += p * max(0, D - |b*D - (B-1)(t - t0)|)
+__global__ void __launch_bounds__(256) k_voxel_acc(int64_t n, const int64_t* __restrict__ t,
+                                                   const uint16_t* __restrict__ x,
+                                                   const uint16_t* __restrict__ y,
+                                                   const int8_t* __restrict__ p, int64_t t0, int64_t t1,
+                                                   int32_t B, int32_t W, int64_t P, long long* acc) {
+  const int64_t D = t1 - t0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ti = t[i];
+    if (ti < t0 || ti >= t1) continue;
+    const int64_t tau = (int64_t)(B - 1) * (ti - t0);
+    const int64_t pix = (int64_t)y[i] * W + x[i];
+    const int64_t b0 = tau / D;  // the two bins that can have weight > 0
+    for (int64_t b = b0; b <= b0 + 1 && b < B; ++b) {
+      int64_t d = b * D - tau;
+      d = d < 0 ? -d : d;
+      const int64_t w = D - d;
+      if (w > 0) atomicAdd(reinterpret_cast<unsigned long long*>(acc + b * P + pix),
+                           (unsigned long long)((int64_t)p[i] * w));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_voxel_finalize(int64_t m, const long long* __restrict__ acc, int64_t D,
+                                                        float* out) {
+  const double inv = 1.0 / (double)D;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (float)((double)acc[i] / (double)D);
+  (void)inv;
+}
+
+// ---- limit_bandwidth -------------------------------------------------------
+// keep[i] = rank of i in its window < cap; per-block kept counts; unsorted flag
+__global__ void __launch_bounds__(1024) k_lb_flags(int64_t n, const int64_t* __restrict__ t, int64_t window,
+                                                   int64_t cap, uint8_t* keep, int64_t* blk, int64_t* flags) {
+  __shared__ int64_t s_scan[33];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t k = 0;
+  if (i < n) {
+    const int64_t t0 = t[0], ti = t[i];
+    if (i > 0 && ti < t[i - 1]) flags[0] = 1;  // model.py:232: requires a timestamp-sorted batch
+    const int64_t w = (ti - t0) / window;
+    const int64_t wstart = t0 + w * window;
+    int64_t lo = 0, hi = i;  // first index with t >= wstart (sorted input)
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (t[mid] < wstart) lo = mid + 1; else hi = mid;
+    }
+    k = (i - lo) < cap ? 1 : 0;
+    keep[i] = (uint8_t)k;
+  }
+  int64_t tot;
+  block_excl_scan<1024, int64_t>(k, s_scan, &tot);
+  if (threadIdx.x == 0) blk[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_blocks(int64_t nb, int64_t* blk, int64_t* total) {
+  __shared__ int64_t s_scan[33];
+  __shared__ int64_t run;
+  if (threadIdx.x == 0) run = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nb; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = i < nb ? blk[i] : 0;
+    int64_t tot;
+    const int64_t ex = block_excl_scan<1024, int64_t>(v, s_scan, &tot);
+    if (i < nb) blk[i] = run + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) run += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) total[0] = run;
+}
+
+__global__ void __launch_bounds__(1024) k_lb_scatter(int64_t n, const int64_t* __restrict__ t,
+                                                     const uint16_t* __restrict__ x,
+                                                     const uint16_t* __restrict__ y,
+                                                     const int8_t* __restrict__ p, const uint8_t* keep,
+                                                     const int64_t* blk, int64_t* ot, uint16_t* ox,
+                                                     uint16_t* oy, int8_t* op) {
+  __shared__ int64_t s_scan[33];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t k = i < n ? keep[i] : 0;
+  int64_t tot;
+  const int64_t ex = block_excl_scan<1024, int64_t>(k, s_scan, &tot);
+  if (k) {
+    const int64_t o = blk[blockIdx.x] + ex;
+    ot[o] = t[i]; ox[o] = x[i]; oy[o] = y[i]; op[o] = p[i];
+  }
+}
+
+}  // namespace evs
+
+using namespace evs;
+
+static inline unsigned grid_for(int64_t n, int64_t cap_blocks) {
+  int64_t b = (n + 255) / 256;
+  if (b > cap_blocks) b = cap_blocks;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+extern "C" {
+
+evs_status evs_accumulate(int64_t n, const int64_t* t, const uint16_t* x, const uint16_t* y, const int8_t* p,
+                          int64_t window_us, int64_t t_end, int32_t width, int32_t height, int64_t* grid,
+                          void* stream) {
+  if (n < 0 || width < 1 || height < 1 || !grid) return EVS_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(grid, 0, sizeof(int64_t) * (size_t)width * height, st) != cudaSuccess) return EVS_ERR_CUDA;
+  if (n > 0)
+    k_accumulate<<<grid_for(n, 148 * 16), 256, 0, st>>>(n, t, x, y, p, t_end - window_us, t_end, width,
+                                                       reinterpret_cast<unsigned long long*>(grid));
+  return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
+}
+
+size_t evs_voxel_workspace_bytes(int32_t bins, int32_t width, int32_t height) {
+  return (size_t)bins * width * height * sizeof(long long);
+}
+
+evs_status evs_voxel(int64_t n, const int64_t* t, const uint16_t* x, const uint16_t* y, const int8_t* p,
+                     int64_t t0, int64_t t1, int32_t bins, int32_t width, int32_t height, float* out,
+                     void* workspace, size_t ws_bytes, void* stream) {
+  if (n < 0 || t1 <= t0 || bins < 2 || width < 1 || height < 1 || !out) return EVS_ERR_ARG;
+  const int64_t P = (int64_t)width * height;
+  if (!workspace || ws_bytes < (size_t)bins * P * sizeof(long long)) return EVS_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  long long* acc = static_cast<long long*>(workspace);
+  if (cudaMemsetAsync(acc, 0, (size_t)bins * P * sizeof(long long), st) != cudaSuccess) return EVS_ERR_CUDA;
+  if (n > 0) k_voxel_acc<<<grid_for(n, 148 * 16), 256, 0, st>>>(n, t, x, y, p, t0, t1, bins, width, P, acc);
+  k_voxel_finalize<<<grid_for((int64_t)bins * P, 148 * 16), 256, 0, st>>>((int64_t)bins * P, acc, t1 - t0, out);
+  return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
+}
+
+size_t evs_limit_bandwidth_workspace_bytes(int64_t n) {
+  const int64_t nb = (n + 1023) / 1024 + 1;
+  return (size_t)n + 16 + (size_t)nb * 8 + 64;
+}
+
+evs_status evs_limit_bandwidth(int64_t n, const int64_t* t, const uint16_t* x, const uint16_t* y,
+                               const int8_t* p, int64_t cap, int64_t window_us, int64_t* ot, uint16_t* ox,
+                               uint16_t* oy, int8_t* op, int64_t* meta_out, void* workspace, size_t ws_bytes,
+                               void* stream) {
+  if (n < 1 || window_us <= 0 || cap < 0 || !meta_out) return EVS_ERR_ARG;
+  if (!workspace || ws_bytes < evs_limit_bandwidth_workspace_bytes(n)) return EVS_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t nb = (n + 1023) / 1024;
+  char* w = static_cast<char*>(workspace);
+  int64_t* blk = reinterpret_cast<int64_t*>(w);
+  uint8_t* keep = reinterpret_cast<uint8_t*>(w + ((nb + 1) * 8 + 63) / 64 * 64);
+  // meta_out: [0] kept count, [1] unsorted flag
+  if (cudaMemsetAsync(meta_out, 0, 2 * sizeof(int64_t), st) != cudaSuccess) return EVS_ERR_CUDA;
+  k_lb_flags<<<(unsigned)nb, 1024, 0, st>>>(n, t, window_us, cap, keep, blk, meta_out + 1);
+  k_scan_blocks<<<1, 1024, 0, st>>>(nb, blk, meta_out);
+  k_lb_scatter<<<(unsigned)nb, 1024, 0, st>>>(n, t, x, y, p, keep, blk, ot, ox, oy, op);
+  return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
+}
+
+}  // extern "C"

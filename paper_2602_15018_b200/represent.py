@@ -70,9 +70,88 @@ def canonical_sort(batch):
     return out.to_host() if was_host else out
 
 
-def accumulate(batch, window_us: int, t_end: int, width: int, height: int) -> np.ndarray:
-    raise NotImplementedError("accumulate: GPU kernel not built yet")
+def accumulate(batch, window_us: int, t_end: int, width: int, height: int, device_output: bool = False):
+    """accumulate_events_to_image (model.py:249-262) on the GPU; int64 (H, W)."""
+    import torch
+
+    _lib.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if len(batch):
+        db, _ = _device_batch(batch)
+        _tmin, _tmax, xm, ym, _badp = batch_stats(db)
+        if xm >= width or ym >= height:  # model.py:253-254
+            raise ValueError("event coordinates out of bounds for the given dimensions")
+    grid = torch.empty((height, width), dtype=torch.int64, device=dev)
+    L = _lib.load()
+    if len(batch) == 0:
+        grid.zero_()
+    else:
+        rc = L.evs_accumulate(len(db), db.t.data_ptr(), db.x.data_ptr(), db.y.data_ptr(), db.polarity.data_ptr(),
+                              int(window_us), int(t_end), int(width), int(height), grid.data_ptr(),
+                              _lib.stream_ptr())
+        _lib.check(rc, "evs_accumulate")
+    return grid if device_output else grid.cpu().numpy()
+
+
+def voxel_grid(batch, t0: int, t1: int, width: int, height: int, bins: int = 5, device_output: bool = False):
+    """Voxel grid of the events with t in [t0, t1) (repo-defined): f32 (bins, H, W)."""
+    import torch
+
+    _lib.require_cuda()
+    if t1 <= t0 or bins < 2:
+        raise ValueError("need t1 > t0 and bins >= 2")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    L = _lib.load()
+    out = torch.empty((bins, height, width), dtype=torch.float32, device=dev)
+    if len(batch):
+        db, _ = _device_batch(batch)
+        _tmin, _tmax, xm, ym, _badp = batch_stats(db)
+        if xm >= width or ym >= height:
+            raise ValueError("event coordinates out of bounds for the given dimensions")
+        n, tp, xp, yp, pp = len(db), db.t.data_ptr(), db.x.data_ptr(), db.y.data_ptr(), db.polarity.data_ptr()
+    else:
+        n, tp, xp, yp, pp = 0, None, None, None, None
+    nbytes = L.evs_voxel_workspace_bytes(bins, width, height)
+    ws, _ep = _workspace(("voxel", dev), nbytes, dev)
+    rc = L.evs_voxel(n, tp, xp, yp, pp, int(t0), int(t1), int(bins), int(width), int(height), out.data_ptr(),
+                     ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+    _lib.check(rc, "evs_voxel")
+    return out if device_output else out.cpu().numpy()
 
 
 def limit_bandwidth(batch, max_events_per_sec: float, window_us: int):
-    raise NotImplementedError("limit_bandwidth: GPU kernel not built yet")
+    """limit_bandwidth (model.py:215-246) on the GPU."""
+    import torch
+
+    if window_us <= 0:
+        raise ValueError("window_us must be positive")
+    if max_events_per_sec < 0:
+        raise ValueError("max_events_per_sec must be >= 0")
+    if len(batch) == 0:
+        if isinstance(batch, DeviceEventBatch):
+            return DeviceEventBatch(batch.t[:0], batch.x[:0], batch.y[:0], batch.polarity[:0],
+                                    batch.dropped_count, True)
+        return EventBatch.empty(dropped_count=batch.dropped_count)
+    _lib.require_cuda()
+    db, was_host = _device_batch(batch)
+    n = len(db)
+    cap = int(max_events_per_sec * window_us * 1e-6)  # model.py:233
+    L = _lib.load()
+    dev = db.t.device
+    ot = torch.empty(n, dtype=torch.int64, device=dev)
+    ox = torch.empty(n, dtype=torch.int16, device=dev)
+    oy = torch.empty(n, dtype=torch.int16, device=dev)
+    op = torch.empty(n, dtype=torch.int8, device=dev)
+    meta = torch.empty(2, dtype=torch.int64, device=dev)
+    ws, _ep = _workspace(("lb", dev), L.evs_limit_bandwidth_workspace_bytes(n), dev)
+    rc = L.evs_limit_bandwidth(n, db.t.data_ptr(), db.x.data_ptr(), db.y.data_ptr(), db.polarity.data_ptr(),
+                               cap, int(window_us), ot.data_ptr(), ox.data_ptr(), oy.data_ptr(), op.data_ptr(),
+                               meta.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+    _lib.check(rc, "evs_limit_bandwidth")
+    kept, unsorted = meta.cpu().tolist()
+    if unsorted:
+        raise ValueError("limit_bandwidth requires a timestamp-sorted batch")
+    out = DeviceEventBatch(ot[:kept], ox[:kept], oy[:kept], op[:kept],
+                           dropped_count=int(batch.dropped_count) + (n - kept),
+                           canonical=getattr(batch, "canonical", False))
+    return out.to_host() if was_host else out
