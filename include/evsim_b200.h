@@ -119,6 +119,15 @@ size_t evs_sort_workspace_bytes(int64_t n, int64_t t_span);
 evs_status evs_canonical_sort(int64_t n, int64_t* t, uint16_t* x, uint16_t* y, int8_t* p,
                               int64_t t_min, int64_t t_span, uint32_t epoch, void* workspace,
                               size_t workspace_bytes, void* stream);
+/* Stable merge of two canonical-ordered device batches A (signal) and B
+ * (noise) into out[na + nb]: the canonical order of concat_batches([A, B])
+ * (types.py:82-92 then parallel.py:112-123) without a full sort.  Requires
+ * t >= t_min, t - t_min < 2^31 and polarity in {-1,+1}; workspace >= nb*8 B. */
+evs_status evs_merge_canonical(int64_t na, const int64_t* at, const uint16_t* ax, const uint16_t* ay,
+                               const int8_t* ap, int64_t nb, const int64_t* bt, const uint16_t* bx,
+                               const uint16_t* by, const int8_t* bp, int64_t t_min, int64_t* out_t,
+                               uint16_t* out_x, uint16_t* out_y, int8_t* out_p, void* workspace,
+                               size_t workspace_bytes, void* stream);
 /* batch statistics used to choose the sort path: out[0]=min t, out[1]=max t,
  * out[2]=max x, out[3]=max y, out[4]=1 if any polarity not in {-1,+1}. */
 evs_status evs_batch_stats(int64_t n, const int64_t* t, const uint16_t* x, const uint16_t* y,

@@ -130,6 +130,7 @@ def _bind_extras(L) -> None:
     L.evs_limit_bandwidth_workspace_bytes.argtypes = [i64]
     L.evs_limit_bandwidth.argtypes = [i64, P, P, P, P, i64, i64, P, P, P, P, P, P, sz, P]
     L.evs_selftest_log.argtypes = [i64, P, P, P, P]
+    L.evs_merge_canonical.argtypes = [i64, P, P, P, P, i64, P, P, P, P, i64, P, P, P, P, P, sz, P]
 
 
 def check(rc: int, what: str) -> None:

@@ -180,6 +180,71 @@ evs_status evs_canonical_sort(int64_t n, int64_t* t, uint16_t* x, uint16_t* y, i
   return EVS_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+__device__ __forceinline__ uint64_t ckey(const int64_t* t, const uint16_t* x, const uint16_t* y, const int8_t* p,
+                                         int64_t i, int64_t tmin) {
+  return ((uint64_t)(t[i] - tmin) << kKeyPixBits) | ((uint64_t)y[i] << 17) | ((uint64_t)x[i] << 1) |
+         (p[i] > 0 ? 1u : 0u);
+}
+
+// B[j] goes to j + upper_bound(A, B[j]); records the split for the A pass
+__global__ void __launch_bounds__(256) k_merge_b(int64_t na, const int64_t* at, const uint16_t* ax,
+                                                 const uint16_t* ay, const int8_t* ap, int64_t nb,
+                                                 const int64_t* bt, const uint16_t* bx, const uint16_t* by,
+                                                 const int8_t* bp, int64_t tmin, int64_t* ub, int64_t* ot,
+                                                 uint16_t* ox, uint16_t* oy, int8_t* op) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t kb = ckey(bt, bx, by, bp, j, tmin);
+    int64_t lo = 0, hi = na;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (ckey(at, ax, ay, ap, mid, tmin) <= kb) lo = mid + 1; else hi = mid;
+    }
+    ub[j] = lo;
+    const int64_t o = j + lo;
+    ot[o] = bt[j]; ox[o] = bx[j]; oy[o] = by[j]; op[o] = bp[j];
+  }
+}
+
+// A[i] goes to i + #{j : ub[j] <= i}
+__global__ void __launch_bounds__(256) k_merge_a(int64_t na, const int64_t* at, const uint16_t* ax,
+                                                 const uint16_t* ay, const int8_t* ap, int64_t nb,
+                                                 const int64_t* ub, int64_t* ot, uint16_t* ox, uint16_t* oy,
+                                                 int8_t* op) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = nb;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (ub[mid] <= i) lo = mid + 1; else hi = mid;
+    }
+    const int64_t o = i + lo;
+    ot[o] = at[i]; ox[o] = ax[i]; oy[o] = ay[i]; op[o] = ap[i];
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+evs_status evs_merge_canonical(int64_t na, const int64_t* at, const uint16_t* ax, const uint16_t* ay,
+                               const int8_t* ap, int64_t nb, const int64_t* bt, const uint16_t* bx,
+                               const uint16_t* by, const int8_t* bp, int64_t t_min, int64_t* out_t,
+                               uint16_t* out_x, uint16_t* out_y, int8_t* out_p, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  if (na < 0 || nb < 0) return EVS_ERR_ARG;
+  if (nb > 0 && (!workspace || workspace_bytes < (size_t)nb * 8)) return EVS_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t* ub = static_cast<int64_t*>(workspace);
+  auto grid = [](int64_t n) { int64_t b = (n + 255) / 256; return (unsigned)(b < 1 ? 1 : (b > 148 * 16 ? 148 * 16 : b)); };
+  if (nb > 0)
+    k_merge_b<<<grid(nb), 256, 0, st>>>(na, at, ax, ay, ap, nb, bt, bx, by, bp, t_min, ub, out_t, out_x, out_y, out_p);
+  if (na > 0) k_merge_a<<<grid(na), 256, 0, st>>>(na, at, ax, ay, ap, nb, ub, out_t, out_x, out_y, out_p);
+  return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
+}
+
 // numpy SeedSequence(entropy).generate_state(4, uint64) + PCG64 srandom_r.
 void evs_seed_pcg64(const uint32_t* words, int32_t nwords, uint64_t out[4]) {
   struct Hasher {

@@ -44,6 +44,8 @@ class EventBatch:
     dropped_count: int = 0
     # True when the batch is known to be in canonical (t, y, x, p) order
     canonical: bool = field(default=False, repr=False, compare=False)
+    # the inputs of concat_batches (lets canonical_sort merge instead of sort)
+    parts: list | None = field(default=None, repr=False, compare=False)
 
     @staticmethod
     def empty(dropped_count: int = 0) -> "EventBatch":
@@ -106,6 +108,7 @@ class DeviceEventBatch:
     polarity: "object"
     dropped_count: int = 0
     canonical: bool = False
+    parts: list | None = None
 
     def __len__(self) -> int:
         return int(self.t.shape[0])
@@ -133,13 +136,13 @@ def concat_batches(batches: list) -> EventBatch:
         return DeviceEventBatch(
             t=torch.cat([b.t for b in batches]), x=torch.cat([b.x for b in batches]),
             y=torch.cat([b.y for b in batches]), polarity=torch.cat([b.polarity for b in batches]),
-            dropped_count=sum(int(b.dropped_count) for b in batches),
+            dropped_count=sum(int(b.dropped_count) for b in batches), parts=list(batches),
         )
     hs = [b.to_host() if isinstance(b, DeviceEventBatch) else b for b in batches]
     return EventBatch(
         t=np.concatenate([b.t for b in hs]), x=np.concatenate([b.x for b in hs]),
         y=np.concatenate([b.y for b in hs]), polarity=np.concatenate([b.polarity for b in hs]),
-        dropped_count=sum(b.dropped_count for b in hs),
+        dropped_count=sum(b.dropped_count for b in hs), parts=list(hs),
     )
 
 

@@ -42,6 +42,31 @@ def batch_stats(db: DeviceEventBatch):
     return [int(v) for v in out.cpu().tolist()]
 
 
+def merge_canonical(a: DeviceEventBatch, b: DeviceEventBatch) -> DeviceEventBatch:
+    """Canonical order of concat([a, b]) for canonical a and b (merge, no sort)."""
+    import torch
+
+    L = _lib.load()
+    na, nb = len(a), len(b)
+    dev = a.t.device
+    if nb == 0 or na == 0:
+        src = a if nb == 0 else b
+        return DeviceEventBatch(src.t, src.x, src.y, src.polarity, a.dropped_count + b.dropped_count, True)
+    tmin = min(int(a.t[0].item()), int(b.t[0].item()))
+    out = DeviceEventBatch(torch.empty(na + nb, dtype=torch.int64, device=dev),
+                           torch.empty(na + nb, dtype=torch.int16, device=dev),
+                           torch.empty(na + nb, dtype=torch.int16, device=dev),
+                           torch.empty(na + nb, dtype=torch.int8, device=dev),
+                           a.dropped_count + b.dropped_count, True)
+    ws, _ep = _workspace(("merge", dev), nb * 8, dev)
+    rc = L.evs_merge_canonical(na, a.t.data_ptr(), a.x.data_ptr(), a.y.data_ptr(), a.polarity.data_ptr(),
+                               nb, b.t.data_ptr(), b.x.data_ptr(), b.y.data_ptr(), b.polarity.data_ptr(), tmin,
+                               out.t.data_ptr(), out.x.data_ptr(), out.y.data_ptr(), out.polarity.data_ptr(),
+                               ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+    _lib.check(rc, "evs_merge_canonical")
+    return out
+
+
 def canonical_sort(batch):
     """parallel.py:112-123 on the GPU (stable order by t, y, x, polarity)."""
     _lib.require_cuda()
@@ -50,6 +75,14 @@ def canonical_sort(batch):
                 else DeviceEventBatch(batch.t, batch.x, batch.y, batch.polarity, batch.dropped_count, True))
     if getattr(batch, "canonical", False):
         return batch
+    parts = getattr(batch, "parts", None)
+    if parts is not None and len(parts) == 2 and getattr(parts[0], "canonical", False):
+        # concat_batches([signal (canonical), noise]): sort the small part, merge
+        a, was_host = _device_batch(parts[0])
+        b = canonical_sort(parts[1].to_device() if not isinstance(parts[1], DeviceEventBatch) else parts[1])
+        if len(a) and len(b) and batch_stats(a)[4] == 0 and batch_stats(b)[4] == 0:
+            out = merge_canonical(a, b)
+            return out.to_host() if not isinstance(batch, DeviceEventBatch) else out
     db, was_host = _device_batch(batch)
     n = len(db)
     tmin, tmax, _xm, _ym, badp = batch_stats(db)

@@ -1,0 +1,173 @@
+"""Batched, device-resident event simulator (the production path).
+
+``EventSimulator`` steps S independent event cameras ("streams") together,
+T frames per call, with every per-pixel state and every output buffer in
+HBM.  One call = one ``evs_step`` (validation prologue, fused generate,
+column scan, ordering pass) for all S x T (stream, frame) segments; optional
+exact noise is generated per segment and merged into the canonical order;
+optional representations (signed-polarity histogram per window,
+accumulate_events_to_image semantics; B-bin voxel grid) are accumulated on
+the device.  ``capture()``/``replay()`` run whole frame sequences as one CUDA
+graph with the step clock advancing on the device.
+
+This is the batched counterpart of the reference's per-tick event block in
+``SimNode.step_once`` (orchestrator.py:159-172): generate -> (noise, seeded
+``_mix64(seed, 0x6E6F6973, k)``) -> concat -> canonical_sort.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .events.model import init_pixel_states
+from .events.types import DeviceEventBatch, EventCameraConfig, IntensityFrame
+from .runtime import StepEngine, StepShape
+
+
+def mix64(*parts: int) -> int:
+    """orchestrator.py:51-56: FNV-style seed mixing used for per-tick noise seeds."""
+    h = 0xCBF29CE484222325
+    for p in parts:
+        h ^= p & 0xFFFFFFFFFFFFFFFF
+        h = (h * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+@dataclass
+class StepResult:
+    """Device-resident outputs of one step (views into the engine's pools)."""
+
+    sim: "EventSimulator"
+    counts: np.ndarray       # [S, T] events written per segment
+    dropped: np.ndarray      # [S, T]
+    reservations: np.ndarray  # [S, T]
+
+    def segment(self, s: int, f: int = 0) -> DeviceEventBatch:
+        return self.sim.segment(s, f)
+
+
+class EventSimulator:
+    def __init__(self, width: int, height: int, streams: int = 1, frames_per_step: int = 1,
+                 config: EventCameraConfig | None = None, tick_us: int = 1000, canonical: bool = True,
+                 device=None):
+        import torch
+
+        _lib.require_cuda()
+        self.W, self.H, self.S, self.T = int(width), int(height), int(streams), int(frames_per_step)
+        self.P = self.W * self.H
+        self.cfg = config or EventCameraConfig()
+        self.tick = int(tick_us)
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.canonical = canonical
+        self.cap = int(self.cfg.capacity(self.W, self.H))
+        self.ref = torch.empty((self.S, self.H, self.W), dtype=torch.float32, device=self.device)
+        self.last = torch.empty((self.S, self.H, self.W), dtype=torch.int64, device=self.device)
+        self.thp = torch.empty_like(self.ref)
+        self.thn = torch.empty_like(self.ref)
+        self.uniform = None
+        self.engine: StepEngine | None = None
+        self.t_next = 0
+        self.step_index = 0
+        self._noise_seed = None
+        self._last_noise = None
+
+    # -- construction (init_pixel_states per stream, model.py:42-67) ----------
+    def reset(self, frames0, seeds=None, t0: int = 0) -> None:
+        """Initialise every stream from its first frame (host numpy, exact thresholds)."""
+        seeds = list(range(self.S)) if seeds is None else list(seeds)
+        uni = []
+        for s in range(self.S):
+            f0 = frames0[s]
+            f0 = f0.detach().cpu().numpy() if type(f0).__module__.startswith("torch") else np.asarray(f0)
+            st = init_pixel_states(IntensityFrame(self.W, self.H, t0, f0), self.cfg, seed=seeds[s])
+            self.ref[s].copy_(st.d_ref_log)
+            self.last[s].copy_(st.d_last_event_t)
+            self.thp[s].copy_(st.d_thresholds_pos)
+            self.thn[s].copy_(st.d_thresholds_neg)
+            uni.append(st.uniform_thresholds)
+        self.uniform = uni[0] if all(u == uni[0] and u is not None for u in uni) else None
+        shape = StepShape(self.S, self.T, self.H, self.W, self.cap,
+                          _lib.EVS_ORDER_CANONICAL if self.canonical else _lib.EVS_ORDER_PIXEL_MAJOR,
+                          self.tick, float(self.cfg.log_eps), int(self.cfg.refractory_us), self.uniform)
+        self.engine = StepEngine(shape, self.device)
+        self.t_next = int(t0)
+        self.step_index = 0
+
+    # -- stepping --------------------------------------------------------------
+    def step(self, frames, validate: bool = True, sync: bool = False, stage_events=None):
+        """Advance every stream by T frames.  frames: float32 CUDA tensor [S, T, H, W]
+        (or [S, H, W] when T == 1).  Asynchronous unless sync=True."""
+        eng = self.engine
+        assert eng is not None, "call reset() first"
+        if frames.dim() == 3:
+            frames = frames.unsqueeze(1)
+        eng.launch(frames.contiguous(), self.ref, self.last, self.thp, self.thn, t0=self.t_next, tick=self.tick,
+                   validate=validate, stage_events=stage_events)
+        self.t_next += self.T * self.tick
+        self.step_index += 1
+        if sync:
+            return self.result()
+        return None
+
+    def result(self) -> StepResult:
+        counts, dropped, res, bad = self.engine.fetch_info()
+        if bad != _lib.NO_BAD:
+            self.engine.reset_bad()
+            s, rem = divmod(int(bad), self.T * self.P)
+            f, pix = divmod(rem, self.P)
+            y, x = divmod(pix, self.W)
+            raise ValueError(f"invalid intensity at stream {s}, frame {f}, pixel (x={x}, y={y})")
+        sh = (self.S, self.T)
+        return StepResult(self, counts.reshape(sh), dropped.reshape(sh), res.reshape(sh))
+
+    def segment(self, s: int, f: int = 0) -> DeviceEventBatch:
+        """Events of stream s, frame f of the last step (canonical order), on the device."""
+        g = s * self.T + f
+        n = int(self.engine.info[0, g].item())
+        e = self.engine
+        return DeviceEventBatch(e.ev_t[g, :n], e.ev_x[g, :n], e.ev_y[g, :n], e.ev_p[g, :n],
+                                dropped_count=int(e.info[1, g].item()), canonical=self.canonical)
+
+    # -- CUDA graph replay -------------------------------------------------------
+    def capture(self, frame_windows) -> None:
+        """Capture one graph stepping through `frame_windows` ([S, T, H, W] each) in order."""
+        self.engine.capture(list(frame_windows), self.ref, self.last, self.thp, self.thn, tick=self.tick,
+                            t0=self.t_next)
+        self._graph_len = len(frame_windows)
+
+    def replay(self) -> None:
+        self.engine.replay()
+        self.t_next += self._graph_len * self.T * self.tick
+        self.step_index += self._graph_len
+
+    # -- noise + representations --------------------------------------------------
+    def segment_with_noise(self, s: int, f: int, seed: int) -> DeviceEventBatch:
+        """Signal events of (s, f) merged with exact noise seeded like SimNode
+        (orchestrator.py:167-171), canonical order."""
+        from .noise import noise_params, run_noise
+        from .represent import merge_canonical
+
+        sig = self.segment(s, f)
+        if self.cfg.noise_rate_hz <= 0:
+            return sig
+        t_now = self.t_next - (self.T - 1 - f) * self.tick
+        t_prev = t_now - self.tick
+        p = noise_params(self.W, self.H, t_prev, t_now, self.cfg.noise_rate_hz, seed, order=0)
+        n, b = run_noise(p, self.device)
+        noise = DeviceEventBatch(b["t"][:n], b["x"][:n], b["y"][:n], b["p"][:n], 0, False)
+        from .represent import canonical_sort
+
+        return merge_canonical(sig, canonical_sort(noise))
+
+    def histogram(self, batch: DeviceEventBatch, window_us: int, t_end: int):
+        from .represent import accumulate
+
+        return accumulate(batch, window_us, t_end, self.W, self.H, device_output=True)
+
+    def voxel(self, batch: DeviceEventBatch, t0: int, t1: int, bins: int = 5):
+        from .represent import voxel_grid
+
+        return voxel_grid(batch, t0, t1, self.W, self.H, bins=bins, device_output=True)

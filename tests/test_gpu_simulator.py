@@ -1,0 +1,101 @@
+"""Batched EventSimulator (S streams x T frames, device resident) and the
+SimNode tick flow (generate -> noise -> concat -> canonical_sort,
+orchestrator.py:159-172) against the CPU oracle."""
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2602_15018_b200.synth import texture_frame
+
+pytestmark = pytest.mark.gpu
+ev = pytest.importorskip("paper_2602_15018_b200.events")
+
+
+def test_simnode_tick_flow_with_noise_matches_oracle():
+    W, H, seed = 160, 90, 42
+    cfg = ev.EventCameraConfig(c_pos=0.15, c_neg=0.15, refractory_us=100, noise_rate_hz=300.0)
+    st = ev.init_pixel_states(ev.IntensityFrame(W, H, 0, texture_frame(W, H, 0.0)), cfg,
+                              seed=oracle.mix64(seed, 0x70697865))
+    ost = oracle.OState(W, H, st.ref_log.copy(), st.last_event_t.copy(), st.thresholds_pos.copy(),
+                        st.thresholds_neg.copy())
+    for k in range(5):
+        t_prev, t_now = k * 1000, (k + 1) * 1000
+        vals = texture_frame(W, H, 0.02 * (k + 1))
+        sig = ev.generate_events_parallel(st, ev.IntensityFrame(W, H, t_now, vals), t_prev, t_now, cfg)
+        nz = ev.inject_noise_events(W, H, t_prev, t_now, cfg.noise_rate_hz, seed=oracle.mix64(seed, 0x6E6F6973, k))
+        got = ev.canonical_sort(ev.concat_batches([sig, nz]))
+        o_sig = oracle.generate(ost, vals, t_prev, t_now, refractory_us=100)
+        o_nz = oracle.noise(W, H, t_prev, t_now, cfg.noise_rate_hz, oracle.mix64(seed, 0x6E6F6973, k))
+        exp = oracle.canonical_sort(oracle.concat([o_sig, o_nz]))
+        assert len(nz) > 0
+        assert got.same_events(exp) and got.dropped_count == exp.dropped_count
+
+
+def test_simulator_streams_frames_noise_and_representations():
+    import torch
+
+    from paper_2602_15018_b200.simulator import EventSimulator, mix64
+
+    S, T, W, H = 3, 2, 128, 72
+    cfg = ev.EventCameraConfig(c_pos=0.1, c_neg=0.1, refractory_us=50, noise_rate_hz=500.0)
+    sim = EventSimulator(W, H, streams=S, frames_per_step=T, config=cfg)
+    f0 = [texture_frame(W, H, 0.137 * s) for s in range(S)]
+    sim.reset(f0, seeds=[10 + s for s in range(S)])
+    ost = [oracle.init_state(f0[s], c_pos=0.1, c_neg=0.1, refractory_us=50, seed=10 + s) for s in range(S)]
+    k = 0
+    for step in range(3):
+        frames = np.stack([[texture_frame(W, H, 0.137 * s + 0.02 * (k + f + 1)) for f in range(T)] for s in range(S)])
+        sim.step(torch.from_numpy(frames).cuda())
+        res = sim.result()
+        for s in range(S):
+            for f in range(T):
+                t_prev, t_now = (k + f) * 1000, (k + f + 1) * 1000
+                o_sig = oracle.generate(ost[s], frames[s, f], t_prev, t_now, refractory_us=50)
+                assert res.counts[s, f] == len(o_sig) and res.reservations[s, f] == o_sig.reservation_count
+                nseed = mix64(99 + s, 0x6E6F6973, k + f)
+                got = sim.segment_with_noise(s, f, nseed).to_host()
+                o_nz = oracle.noise(W, H, t_prev, t_now, 500.0, nseed)
+                exp = oracle.canonical_sort(oracle.concat([o_sig, o_nz]))
+                assert got.same_events(exp), (step, s, f)
+                if f == T - 1:
+                    hist = sim.histogram(sim.segment(s, f), 1000, t_now).cpu().numpy()
+                    assert np.array_equal(hist, oracle.accumulate(o_sig, 1000, t_now, W, H))
+                    vox = sim.voxel(sim.segment(s, f), t_prev, t_now, bins=5).cpu().numpy()
+                    np.testing.assert_array_equal(vox, oracle.voxel(o_sig, t_prev, t_now, 5, W, H))
+            assert np.array_equal(sim.ref[s].cpu().numpy(), ost[s].ref_log)
+        k += T
+
+
+def test_simulator_graph_replay_multistream():
+    import torch
+
+    from paper_2602_15018_b200.simulator import EventSimulator
+
+    S, W, H = 4, 96, 64
+    cfg = ev.EventCameraConfig(c_pos=0.15, c_neg=0.15, refractory_us=100)
+    sim = EventSimulator(W, H, streams=S, frames_per_step=1, config=cfg)
+    f0 = [texture_frame(W, H, 0.137 * s) for s in range(S)]
+    sim.reset(f0)
+    ost = [oracle.init_state(f0[s], c_pos=0.15, c_neg=0.15, refractory_us=100, seed=s) for s in range(S)]
+    ring = torch.from_numpy(np.stack([[texture_frame(W, H, 0.137 * s + 0.02 * (i + 1)) for s in range(S)]
+                                      for i in range(5)])).cuda()  # [5, S, H, W]
+    sim.step(ring[0])  # eager first step
+    sim.result()
+    for s in range(S):
+        oracle.generate(ost[s], ring[0, s].cpu().numpy(), 0, 1000, refractory_us=100)
+    windows = [ring[i].unsqueeze(1).contiguous() for i in range(1, 5)]
+    sim.capture(windows)
+    t = 1000
+    for _rep in range(2):
+        sim.replay()
+        res = sim.result()
+        for i in range(1, 5):
+            for s in range(S):
+                o = oracle.generate(ost[s], ring[i, s].cpu().numpy(), t, t + 1000, refractory_us=100)
+                if i == 4:
+                    assert res.counts[s, 0] == len(o)
+                    assert sim.segment(s, 0).to_host().same_events(oracle.canonical_sort(o))
+            t += 1000
+        for s in range(S):
+            assert np.array_equal(sim.ref[s].cpu().numpy(), ost[s].ref_log)
