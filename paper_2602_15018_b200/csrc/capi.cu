@@ -1,4 +1,10 @@
 // extern "C" entry points of libevsim_b200.so (see include/evsim_b200.h).
+//
+// One evs_step = k_prologue (validate + clock + counters) -> k_generate (K1,
+// per-tile event regions) -> k_tilescan (tile bases, counts, capacity, column
+// scan of the t_rel histogram rows) -> k_tile_order (K2: canonical order, or
+// pixel-major compaction for the serial API) [-> generic onesweep passes when
+// t_now - t_prev exceeds 2^11 us].
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -27,11 +33,10 @@ int sm_count_current() {
 }
 
 struct StepLayout {
-  int nseg, ntiles1, npass, bits, NB, ngroups;
-  size_t rows, group_base, tot;
-  int64_t max_tiles2;
-  size_t ctr, desc, status1, hist, gstart, seg_total, seg_tbase, seg_tile_prefix, status2, keysA, keysB,
-      total;
+  int nseg, ntiles, npass, bits, NB, ngroups, gt;
+  int64_t max_tiles2, ovf_cap;
+  size_t ctr, desc, zero2, region, tile_count, tile_ovf, tile_base, ovf_area, rows, tot, hist, gstart,
+      seg_tbase, seg_tile_prefix, status2, keysA, keysB, total;
 };
 
 __global__ void k_clock_init(StepDesc* d, int64_t t0, uint32_t epoch) {
@@ -43,14 +48,14 @@ __global__ void k_clock_init(StepDesc* d, int64_t t0, uint32_t epoch) {
 
 bool step_layout(const evs_step_params* p, StepLayout* L) {
   if (!p || p->streams < 1 || p->frames < 1 || p->height < 1 || p->width < 1) return false;
-  if (p->height > 65535 || p->width > 65535) return false;
+  if (p->height > 65535 || p->width > 65535 || p->capacity < 0) return false;
   const int64_t P = (int64_t)p->height * p->width;
   L->nseg = p->streams * p->frames;
-  L->ntiles1 = (int)((P + kGenTile - 1) / kGenTile);
+  L->ntiles = (int)((P + kGenTile - 1) / kGenTile);
   const bool canon = p->order == EVS_ORDER_CANONICAL;
   int tbits = 1;
   if (canon) {
-    int64_t mdt = p->max_dt > 0 ? p->max_dt : p->tick;
+    const int64_t mdt = p->max_dt > 0 ? p->max_dt : p->tick;
     if (mdt <= 0 || mdt >= (1ll << 31)) return false;
     tbits = ilog2_ceil((uint64_t)mdt);
     if (tbits < 1) tbits = 1;
@@ -58,24 +63,36 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   L->npass = canon ? (tbits + kMaxDigitBits - 1) / kMaxDigitBits : 0;
   L->bits = canon ? (tbits + L->npass - 1) / L->npass : 0;
   L->NB = canon ? (1 << L->bits) : 0;
-  // generic onesweep passes (k_order) only for t_rel wider than one digit
   L->max_tiles2 = (canon && L->npass > 1) ? (p->capacity + kOrdTile - 1) / kOrdTile : 0;
-  L->ngroups = (L->ntiles1 + kGroupTiles - 1) / kGroupTiles;
+  // tiles per histogram row / K2 CTA: as large as possible (fewer rows, longer
+  // K2 chunks) while keeping >= 2 K2 CTAs per SM over the whole batch
+  L->gt = 1;
+  while (L->gt < kMaxGroupTiles &&
+         (int64_t)((L->ntiles + 2 * L->gt - 1) / (2 * L->gt)) * L->nseg >= 2 * 148)
+    L->gt *= 2;
+  L->ngroups = (L->ntiles + L->gt - 1) / L->gt;
+  // overflow area (lanes with > kSlotsPerLane events): the kept events of a
+  // frame never exceed the capacity, so capacity + one tile is always enough
+  L->ovf_cap = p->capacity + (int64_t)kTileCap * (1 + L->ntiles / 4);
+  const size_t ns = (size_t)L->nseg, nt = (size_t)L->ntiles;
   size_t off = 0;
   L->ctr = off; off = align_up(off + 64 * sizeof(uint32_t));
   L->desc = off; off = align_up(off + sizeof(StepDesc));
-  L->status1 = off; off = align_up(off + (size_t)L->nseg * L->ntiles1 * 8);
-  L->rows = off; off = align_up(off + (canon ? (size_t)L->nseg * L->ngroups * L->NB * 4 : 0));
-  L->group_base = off; off = align_up(off + (size_t)L->nseg * L->ngroups * 8);
-  L->tot = off; off = align_up(off + (size_t)L->nseg * L->NB * 4);
-  L->hist = off; off = align_up(off + (L->npass > 1 ? (size_t)L->nseg * L->npass * kHistReps * L->NB * 4 : 0));
-  L->gstart = off; off = align_up(off + (size_t)L->nseg * L->NB * 4);
-  L->seg_total = off; off = align_up(off + (size_t)L->nseg * 8);
-  L->seg_tbase = off; off = align_up(off + (size_t)L->nseg * 8);
-  L->seg_tile_prefix = off; off = align_up(off + (size_t)(L->nseg + 1) * 4);
-  L->status2 = off; off = align_up(off + (size_t)L->nseg * L->max_tiles2 * L->NB * 8);
-  L->keysA = off; off = align_up(off + (canon ? (size_t)L->nseg * p->capacity * 8 : 0));
-  L->keysB = off; off = align_up(off + (canon && L->npass > 1 ? (size_t)L->nseg * p->capacity * 8 : 0));
+  L->zero2 = off; off = align_up(off + (ns + 1) * 8);  // ovf_cursor[nseg] + err
+  L->tile_count = off; off = align_up(off + ns * nt * 8);
+  L->tile_ovf = off; off = align_up(off + ns * nt * 8);
+  L->tile_base = off; off = align_up(off + ns * nt * 8);
+  L->seg_tbase = off; off = align_up(off + ns * 8);
+  L->rows = off; off = align_up(off + (canon ? ns * L->ngroups * L->NB * 4 : 0));
+  L->tot = off; off = align_up(off + ns * L->NB * 4);
+  L->hist = off; off = align_up(off + (L->npass > 1 ? ns * L->npass * kHistReps * L->NB * 4 : 0));
+  L->gstart = off; off = align_up(off + ns * L->NB * 4);
+  L->seg_tile_prefix = off; off = align_up(off + (ns + 1) * 4);
+  L->status2 = off; off = align_up(off + ns * L->max_tiles2 * L->NB * 8);
+  L->keysA = off; off = align_up(off + (canon && L->npass > 1 ? ns * p->capacity * 8 : 0));
+  L->keysB = off; off = align_up(off + (canon && L->npass > 1 ? ns * p->capacity * 8 : 0));
+  L->region = off; off = align_up(off + ns * nt * kTileCap * 8);
+  L->ovf_area = off; off = align_up(off + ns * (size_t)L->ovf_cap * 8);
   L->total = off;
   return true;
 }
@@ -87,7 +104,7 @@ T* at(void* ws, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(ws)
 
 extern "C" {
 
-int evs_version(void) { return 1; }
+int evs_version(void) { return 2; }
 
 const char* evs_error_string(evs_status code) {
   switch (code) {
@@ -110,8 +127,7 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
                             size_t ws_bytes, void* stream, void* const* evs, int nev) {
   StepLayout L;
   if (!step_layout(p, &L) || !b) return EVS_ERR_ARG;
-  if (p->log_eps <= 0 || p->refractory_us < 0 || p->capacity < 0 || p->capacity >= (1ll << 32))
-    return EVS_ERR_ARG;
+  if (p->log_eps <= 0 || p->refractory_us < 0 || p->capacity >= (1ll << 32)) return EVS_ERR_ARG;
   if (!b->frames || !b->ref_log || !b->last_event_t || !b->counts || !b->dropped ||
       !b->reservations || !b->bad_pixel)
     return EVS_ERR_ARG;
@@ -126,81 +142,77 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   if (p->capacity > 0 && (!b->ev_t || !b->ev_x || !b->ev_y || !b->ev_p)) return EVS_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t P = (int64_t)p->height * p->width;
-
   auto mark = [&](int i) {
     if (evs && i < nev && evs[i]) cudaEventRecord(static_cast<cudaEvent_t>(evs[i]), st);
   };
+  int64_t* zero2 = at<int64_t>(ws, L.zero2);
+
   mark(0);
   cudaError_t e = launch_prologue(b->frames, (int64_t)L.nseg * P, P, p->validate, b->bad_pixel,
-                                  b->reservations, L.nseg, desc, (int64_t)p->frames * p->tick, st);
+                                  b->reservations, L.nseg, desc, (int64_t)p->frames * p->tick, zero2,
+                                  L.nseg + 1, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(1);
 
   GenArgs g;
   memset(&g, 0, sizeof(g));
   g.S = p->streams; g.T = p->frames; g.H = p->height; g.W = p->width; g.P = P;
-  g.log_eps = p->log_eps; g.refr = p->refractory_us; g.cap = p->capacity;
+  g.log_eps = p->log_eps; g.log_eps_f = (float)p->log_eps;
+  g.refr = p->refractory_us; g.cap = p->capacity;
   g.thp_u = p->th_pos_uniform; g.thn_u = p->th_neg_uniform;
   g.frames = b->frames; g.t_bounds = b->t_bounds; g.t0 = p->t0; g.tick = p->tick;
   g.ref = b->ref_log; g.last = b->last_event_t; g.thp = b->th_pos; g.thn = b->th_neg;
-  g.mode = canon ? 1 : 0;
-  g.out_t = b->ev_t; g.out_x = b->ev_x; g.out_y = b->ev_y; g.out_p = b->ev_p;
-  g.keys = canon ? at<uint64_t>(ws, L.keysA) : nullptr;
-  g.seg_stride = p->capacity;
-  g.seg_total = at<int64_t>(ws, L.seg_total);
   g.seg_res = b->reservations;
   g.seg_tbase = at<int64_t>(ws, L.seg_tbase);
-  g.hist = nullptr;
-  g.npass = L.npass; g.hist_bits = L.bits;
-  g.status = at<uint64_t>(ws, L.status1);
-  g.tile_ctr = at<uint32_t>(ws, L.ctr);
+  g.hist_bits = L.bits;
   g.bad = b->bad_pixel;
   g.epoch = p->epoch;
-  g.ntiles = L.ntiles1;
+  g.ntiles = L.ntiles;
   g.desc = desc;
   g.rows = canon ? at<uint32_t>(ws, L.rows) : nullptr;
-  g.group_base = canon ? at<int64_t>(ws, L.group_base) : nullptr;
   g.ngroups = L.ngroups;
-  g.log_eps_f = (float)p->log_eps;
+  g.gt = L.gt;
+  g.region = at<uint64_t>(ws, L.region);
+  g.tile_count = at<int64_t>(ws, L.tile_count);
+  g.tile_ovf = at<int64_t>(ws, L.tile_ovf);
+  g.ovf_area = at<uint64_t>(ws, L.ovf_area);
+  g.ovf_cursor = reinterpret_cast<unsigned long long*>(zero2);
+  g.ovf_cap = L.ovf_cap;
+  g.err = zero2 + L.nseg;
   e = launch_generate(g, b->th_pos == nullptr, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(2);
 
-  if (!canon) {
-    PlanArgs pl;
-    memset(&pl, 0, sizeof(pl));
-    pl.nseg = L.nseg; pl.cap = p->capacity; pl.seg_total = g.seg_total;
-    pl.out_count = b->counts; pl.out_dropped = b->dropped;
-    pl.bad = b->bad_pixel;
-    e = launch_plan(pl, st);
-    if (e != cudaSuccess) return EVS_ERR_CUDA;
-    mark(3);
-    mark(4);
-    return EVS_OK;
-  }
-
-  // pass 0 (lowest t_rel digit): column scan of the K1 group rows + group-CTA ordering
-  ColScanArgs cs;
-  cs.nseg = L.nseg; cs.ngroups = L.ngroups; cs.bits = L.bits; cs.cap = p->capacity;
-  cs.rows = g.rows; cs.tot = at<uint32_t>(ws, L.tot); cs.seg_total = g.seg_total;
-  cs.out_count = b->counts; cs.out_dropped = b->dropped; cs.bad = b->bad_pixel;
-  e = launch_colscan(cs, st);
+  TileScanArgs ts;
+  memset(&ts, 0, sizeof(ts));
+  ts.nseg = L.nseg; ts.ntiles = L.ntiles; ts.ngroups = L.ngroups; ts.bits = L.bits; ts.cap = p->capacity;
+  ts.gt = L.gt;
+  ts.tile_count = g.tile_count; ts.tile_ovf = g.tile_ovf; ts.region = g.region; ts.ovf_area = g.ovf_area;
+  ts.ovf_cap = L.ovf_cap; ts.tile_base = at<int64_t>(ws, L.tile_base);
+  ts.rows = g.rows; ts.tot = at<uint32_t>(ws, L.tot);
+  ts.out_count = b->counts; ts.out_dropped = b->dropped; ts.bad = b->bad_pixel; ts.err = g.err;
+  e = launch_tilescan(ts, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(3);
-  GroupOrderArgs go;
-  go.nseg = L.nseg; go.ngroups = L.ngroups; go.bits = L.bits; go.shift = kKeyPixBits;
-  go.keys_in = at<uint64_t>(ws, L.keysA); go.seg_stride = p->capacity;
-  go.rows = g.rows; go.tot = cs.tot; go.group_base = g.group_base; go.seg_count = b->counts;
-  go.final_soa = L.npass == 1; go.keys_out = at<uint64_t>(ws, L.keysB);
-  go.out_t = b->ev_t; go.out_x = b->ev_x; go.out_y = b->ev_y; go.out_p = b->ev_p;
-  go.seg_tbase = g.seg_tbase;
-  e = launch_group_order(go, st);
+
+  TileOrderArgs to;
+  memset(&to, 0, sizeof(to));
+  to.nseg = L.nseg; to.ntiles = L.ntiles; to.ngroups = L.ngroups; to.bits = L.bits; to.shift = kKeyPixBits;
+  to.gt = L.gt;
+  to.cap = p->capacity; to.tile_count = g.tile_count; to.tile_ovf = g.tile_ovf; to.tile_base = ts.tile_base;
+  to.region = g.region; to.ovf_area = g.ovf_area; to.ovf_cap = L.ovf_cap; to.rows = g.rows; to.tot = ts.tot;
+  to.seg_stride = p->capacity; to.pixel_major = canon ? 0 : 1;
+  to.final_soa = (!canon || L.npass == 1) ? 1 : 0;
+  to.keys_out = at<uint64_t>(ws, L.keysB);
+  to.out_t = b->ev_t; to.out_x = b->ev_x; to.out_y = b->ev_y; to.out_p = b->ev_p;
+  to.seg_tbase = g.seg_tbase; to.bad = b->bad_pixel;
+  e = launch_tile_order(to, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
 
-  if (L.npass > 1) {
+  if (canon && L.npass > 1) {
     // wide t_rel (dt > 2^11 us): remaining digits with generic onesweep passes
     HistArgs h;
-    h.nseg = L.nseg; h.keys = go.keys_out; h.seg_stride = p->capacity; h.seg_count = b->counts;
+    h.nseg = L.nseg; h.keys = to.keys_out; h.seg_stride = p->capacity; h.seg_count = b->counts;
     h.npass = L.npass; h.pass0 = 1; h.bits = L.bits; h.base_shift = kKeyPixBits;
     h.hist = at<uint32_t>(ws, L.hist);
     e = launch_hist(h, st);
@@ -209,7 +221,7 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
     for (int pass = 1; pass < L.npass; ++pass) {
       PlanArgs pl;
       memset(&pl, 0, sizeof(pl));
-      pl.nseg = L.nseg; pl.cap = p->capacity; pl.seg_total = g.seg_total;
+      pl.nseg = L.nseg; pl.cap = p->capacity; pl.seg_total = b->counts;
       pl.hist = h.hist; pl.npass = L.npass; pl.pass = pass; pl.bits = L.bits;
       pl.gstart = at<uint32_t>(ws, L.gstart);
       pl.seg_tile_prefix = at<uint32_t>(ws, L.seg_tile_prefix);
@@ -244,6 +256,12 @@ evs_status evs_step(const evs_step_params* p, const evs_step_buffers* b, void* w
   return step_impl(p, b, ws, ws_bytes, stream, nullptr, 0);
 }
 
+evs_status evs_step_profiled(const evs_step_params* p, const evs_step_buffers* b, void* ws,
+                             size_t ws_bytes, void* stream, void* const* stage_events,
+                             int32_t n_events) {
+  return step_impl(p, b, ws, ws_bytes, stream, stage_events, n_events);
+}
+
 evs_status evs_selftest_log(int64_t n, const double* x, double* out_fast, double* out_cuda, void* stream) {
   if (n < 0 || (n > 0 && (!x || !out_fast || !out_cuda))) return EVS_ERR_ARG;
   return launch_selftest_log(x, out_fast, out_cuda, n, static_cast<cudaStream_t>(stream)) == cudaSuccess
@@ -258,12 +276,6 @@ evs_status evs_step_clock_init(const evs_step_params* p, void* ws, size_t ws_byt
   if (epoch == 0 || epoch + EVS_EPOCHS_PER_CALL > EVS_EPOCH_LIMIT) return EVS_ERR_ARG;
   k_clock_init<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(at<StepDesc>(ws, L.desc), t0, epoch);
   return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
-}
-
-evs_status evs_step_profiled(const evs_step_params* p, const evs_step_buffers* b, void* ws,
-                             size_t ws_bytes, void* stream, void* const* stage_events,
-                             int32_t n_events) {
-  return step_impl(p, b, ws, ws_bytes, stream, stage_events, n_events);
 }
 
 }  // extern "C"

@@ -1,0 +1,752 @@
+// K1 -- fused event generation for sm_100a (the reference's lane math,
+// model.py:79-171 == parallel.py:126-273, for S streams x T frames).
+//
+// Per pixel (thread-owned, state held in registers across the T frames):
+//   * f32 prefilter certifies "no crossing" (n == 0) without any FP64 work;
+//   * f64 log via a 128-entry table + compensated degree-8 log1p (<= 1 ulp,
+//     model.py:39), f64 diff against the f32 reference level;
+//   * crossing count n = floor(|diff|/th + 1e-4) and event times
+//     floor(((j*th)/|diff|)*dt) via reciprocals, falling back to the exact
+//     IEEE division whenever the floor could differ (model.py:137, :144);
+//   * refractory filter against last_event_t (model.py:148-150);
+//   * state update ref = f32(ref + pol*n*th), last_event_t (model.py:159-163).
+// Per tile: warp ballot per 32-pixel chunk (AggregationStats.reservation_count),
+// block scan of the per-lane counts, decoupled lookback (wide windows) for the
+// tile's pixel-major base, capacity cut at the first `cap` events
+// (model.py:150-158), smem-staged coalesced writes, and a per-tile-group
+// t_rel histogram row for the ordering pass (order.cu).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "log_table.h"
+
+namespace evs {
+
+struct LogTab {
+  double c[128], invc[128], lh[128], ll[128];
+};
+
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  const double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
+}
+
+// log(x) for x > 0, <= 1 ulp (tools/gen_log_table.py documents the table).
+__device__ __forceinline__ double fast_log(double x, const LogTab& T) {
+  const uint64_t ix = (uint64_t)__double_as_longlong(x);
+  if (ix < 0x0010000000000000ull || ix >= 0x7ff0000000000000ull) return log(x);  // subnormal / inf / nan
+  const uint64_t tmp = ix - kLogOff;
+  const int i = (int)((tmp >> (52 - kLogTableBits)) & ((1u << kLogTableBits) - 1));
+  const int k = (int)((int64_t)tmp >> 52);
+  const double z = __longlong_as_double((long long)(ix - (tmp & 0xfff0000000000000ull)));
+  const double c = T.c[i], invc = T.invc[i];
+  const double d = z - c;  // exact (Sterbenz)
+  const double rh = d * invc;
+  const double rl = fma(-rh, c, d) * invc;  // r = rh + rl = (z - c) / c
+  double q = -0.125;
+  q = fma(q, rh, 1.0 / 7.0);
+  q = fma(q, rh, -1.0 / 6.0);
+  q = fma(q, rh, 0.2);
+  q = fma(q, rh, -0.25);
+  q = fma(q, rh, 1.0 / 3.0);
+  q = fma(q, rh, -0.5);
+  const double kd = (double)k;
+  double s1, e1, s2, e2;
+  two_sum(kd * kLn2Hi, T.lh[i], s1, e1);
+  two_sum(s1, rh, s2, e2);
+  double lo = e1 + e2 + (kd * kLn2Lo + T.ll[i]) + rl;
+  lo = fma(rh * rh, q, lo);
+  return s2 + lo;
+}
+
+// Newton-refined reciprocal (~1 ulp); only used where results are checked.
+__device__ __forceinline__ double rcp_nr(double a) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  double e = fma(-a, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-a, y, 1.0);
+  y = fma(y, e, y);
+  return y;
+}
+
+// floor(v) of a value whose approximation `va` is within ~8 ulp; returns -1
+// when an integer lies within the error band (caller then computes exactly).
+__device__ __forceinline__ int64_t safe_floor(double va) {
+  const double fl = floor(va);
+  const double tol = va * 4e-15 + 1e-290;
+  if (va - fl < tol || fl + 1.0 - va < tol) return -1;
+  return (int64_t)fl;
+}
+
+__device__ __forceinline__ int64_t t_rel_exact(int j, double thd, double adiff, double dtd, int64_t dt) {
+  // model.py:144-146: int(((j*th)/|diff|)*dt), clamped to dt-1 (IEEE division)
+  int64_t tr = (int64_t)((((double)j * thd) / adiff) * dtd);
+  return tr > dt - 1 ? dt - 1 : tr;
+}
+
+__device__ __forceinline__ int64_t t_rel_fast(int j, double thd, double adiff, double ra, double dtd, int64_t dt) {
+  const int64_t f = safe_floor(((double)j * thd) * ra * dtd);
+  if (f < 0) return t_rel_exact(j, thd, adiff, dtd, dt);
+  return f > dt - 1 ? dt - 1 : f;
+}
+
+template <int MODE>
+__device__ __forceinline__ void put_event(const GenArgs& a, int64_t segoff, int64_t g, uint64_t key,
+                                          int64_t tprev) {
+  if (MODE == 0) {
+    a.out_t[segoff + g] = tprev + (int64_t)(key >> kKeyPixBits);
+    a.out_x[segoff + g] = (uint16_t)((key >> 1) & 0xffffu);
+    a.out_y[segoff + g] = (uint16_t)((key >> 17) & 0xffffu);
+    a.out_p[segoff + g] = (key & 1u) ? (int8_t)1 : (int8_t)-1;
+  } else {
+    a.keys[segoff + g] = key;
+  }
+}
+
+// Per-step constants of the lane math.
+struct LaneCtx {
+  double log_eps, rth_pos, rth_neg, dtd;
+  int64_t tprev, dt, refr;
+  float log_eps_f;
+};
+
+// One pixel of one frame (model.py:124-163).  Calls sink(key) for every
+// refractory-surviving event in emission order (chronological), returns the
+// number of such events, and produces the new (ref, last) in r_new / lt_new.
+template <bool REFR, bool UNI, typename Sink>
+__device__ __forceinline__ int lane_pixel(float v, float r, int64_t lt, float thp, float thn, uint64_t xy,
+                                          const LaneCtx& c, const LogTab& T, float& r_new, int64_t& lt_new,
+                                          Sink&& sink) {
+  r_new = r;
+  lt_new = lt;
+  {
+    // f32 prefilter: |__logf - ln| <= 2^-21 |ln| + 2^-22 and the f32 rounding of
+    // v + eps are far inside the margin, so a pixel is skipped only when
+    // |diff| < th (1 - 1e-4) surely holds (then n == 0: no event, no change).
+    const float lf = __logf(v + c.log_eps_f);
+    const float d32 = lf - r;
+    const float th32 = d32 > 0.f ? thp : thn;
+    if (fabsf(d32) + (2e-6f * fabsf(lf) + 2e-6f) < th32 * (1.0f - 1e-4f)) return 0;
+  }
+  const double ln = fast_log((double)v + c.log_eps, T);  // model.py:39 (f64)
+  const double ls = (double)r;
+  const double diff = ln - ls;
+  if (diff == 0.0) return 0;
+  const bool pos = diff > 0.0;
+  const float th = pos ? thp : thn;
+  const double thd = (double)th;
+  const double ad = pos ? diff : -diff;
+  // n = int(|diff|/th + 1e-4) (model.py:137)
+  const double rth = UNI ? (pos ? c.rth_pos : c.rth_neg) : rcp_nr(thd);
+  int64_t n64 = safe_floor(fma(ad, rth, 1e-4));
+  if (n64 < 0) n64 = (int64_t)(ad / thd + 1e-4);
+  if (n64 <= 0) return 0;
+  const int n = n64 > 2147483647 ? 2147483647 : (int)n64;
+  // t_rel(j) = int(((j*th)/|diff|)*dt) (model.py:144): j * u, exact fallback
+  // whenever the floor of the approximation could differ from the reference's
+  const double u = thd * rcp_nr(ad) * c.dtd;
+  const uint64_t xyp = xy | (pos ? 1u : 0u);
+  int kept = 0;
+  int64_t l = lt;
+  for (int j = 1; j <= n; ++j) {
+    int64_t tr = safe_floor((double)j * u);
+    if (tr < 0) tr = (int64_t)((((double)j * thd) / ad) * c.dtd);
+    if (tr > c.dt - 1) tr = c.dt - 1;  // model.py:145-146
+    if (REFR) {
+      if (c.tprev + tr - l < c.refr) continue;  // model.py:148-149
+    }
+    l = c.tprev + tr;
+    sink(((uint64_t)tr << kKeyPixBits) | xyp, kept);
+    ++kept;
+  }
+  lt_new = l;
+  const double step = (double)n * thd;          // exact in f64
+  r_new = (float)(pos ? ls + step : ls - step);  // model.py:159-162
+  return kept;
+}
+
+constexpr int kSlots = 16;  // per-lane event slots in smem (4 events per pixel)
+
+// self-test: the fast log and CUDA's log side by side (tests/test_gpu_fastlog.py)
+__global__ void k_selftest_log(const double* x, double* out_fast, double* out_ref, int64_t n) {
+  __shared__ LogTab s_log;
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) {
+    s_log.c[i] = kLogTable[i][0];
+    s_log.invc[i] = kLogTable[i][1];
+    s_log.lh[i] = kLogTable[i][2];
+    s_log.ll[i] = kLogTable[i][3];
+  }
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    out_fast[i] = fast_log(x[i], s_log);
+    out_ref[i] = log(x[i]);
+  }
+}
+
+cudaError_t launch_selftest_log(const double* x, double* out_fast, double* out_ref, int64_t n, cudaStream_t st) {
+  k_selftest_log<<<1024, 256, 0, st>>>(x, out_fast, out_ref, n);
+  return cudaGetLastError();
+}
+
+template <typename K>
+static void ensure_smem_gen(K k) {
+  static const void* done[32];
+  static int ndone = 0;
+  const void* key = reinterpret_cast<const void*>(k);
+  for (int i = 0; i < ndone; ++i)
+    if (done[i] == key) return;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  if (ndone < 32) done[ndone++] = key;
+}
+
+// K1 tile: 256 lanes x 4 pixels.  No inter-tile dependency: the tile's events
+// (pixel-major) go to its own region; k_tilescan later turns the per-tile
+// counts into pixel-major bases and applies the capacity cut.
+template <bool VEC, bool REFR, bool UNI>
+__global__ void __launch_bounds__(kGenThreads, 3) k_generate(GenArgs a) {
+  constexpr int NT = kGenThreads, VPT = kGenVpt, TILE = kGenTile, NW = NT / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* slots = reinterpret_cast<uint64_t*>(smem_raw);  // [kSlots][NT] (slot-major: conflict free)
+  uint64_t* stg = slots + kSlots * NT;                       // [kTileCap] compacted tile events
+  __shared__ LogTab s_log;
+  __shared__ int64_t s_scan[NW + 1];
+  __shared__ long long s_off;
+  __shared__ int s_res;
+
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int s = (int)(blockIdx.x / (uint32_t)a.ntiles);
+  const int tile = (int)(blockIdx.x % (uint32_t)a.ntiles);
+  const int64_t P = a.P;
+  const int64_t pix0 = (int64_t)tile * TILE + (int64_t)tid * VPT;
+  const bool full = VEC && (pix0 + VPT <= P);
+  float* refp = a.ref + (int64_t)s * P;
+  int64_t* lastp = a.last + (int64_t)s * P;
+
+  float r[VPT], thp[VPT], thn[VPT];
+  int64_t lt[VPT];
+  bool dirty[VPT];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) { r[k] = 0.f; lt[k] = 0; dirty[k] = false; thp[k] = a.thp_u; thn[k] = a.thn_u; }
+  if (full) {
+    float4 q = *reinterpret_cast<const float4*>(refp + pix0);
+    r[0] = q.x; r[1] = q.y; r[2] = q.z; r[3] = q.w;
+    if (REFR) {
+      longlong2 l0 = *reinterpret_cast<const longlong2*>(lastp + pix0);
+      longlong2 l1 = *reinterpret_cast<const longlong2*>(lastp + pix0 + 2);
+      lt[0] = l0.x; lt[1] = l0.y; lt[2] = l1.x; lt[3] = l1.y;
+    }
+    if (!UNI) {
+      float4 p4 = *reinterpret_cast<const float4*>(a.thp + (int64_t)s * P + pix0);
+      float4 n4 = *reinterpret_cast<const float4*>(a.thn + (int64_t)s * P + pix0);
+      thp[0] = p4.x; thp[1] = p4.y; thp[2] = p4.z; thp[3] = p4.w;
+      thn[0] = n4.x; thn[1] = n4.y; thn[2] = n4.z; thn[3] = n4.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      if (pix0 + k < P) {
+        r[k] = refp[pix0 + k];
+        if (REFR) lt[k] = lastp[pix0 + k];
+        if (!UNI) { thp[k] = a.thp[(int64_t)s * P + pix0 + k]; thn[k] = a.thn[(int64_t)s * P + pix0 + k]; }
+      }
+    }
+  }
+  const int64_t clock_t0 = a.desc ? a.desc->cur_t0 : a.t0;
+  if (tid < 128) {
+    s_log.c[tid] = kLogTable[tid][0];
+    s_log.invc[tid] = kLogTable[tid][1];
+    s_log.lh[tid] = kLogTable[tid][2];
+    s_log.ll[tid] = kLogTable[tid][3];
+  }
+  if (tid == 0) s_res = 0;
+  uint64_t xyk[VPT];
+  {
+    const uint32_t W = (uint32_t)a.W;
+    uint32_t y = (uint32_t)pix0 / W;
+    uint32_t x = (uint32_t)pix0 - y * W;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      xyk[k] = ((uint64_t)y << 17) | ((uint64_t)x << 1);
+      if (++x == W) { x = 0; ++y; }
+    }
+  }
+  const int NB = a.rows ? (1 << a.hist_bits) : 0;
+  __syncthreads();
+
+  LaneCtx c;
+  c.log_eps = a.log_eps; c.log_eps_f = a.log_eps_f; c.rth_pos = a.rth_pos; c.rth_neg = a.rth_neg;
+  c.refr = a.refr;
+
+  // frame values are prefetched one frame ahead (registers) so the next
+  // frame's HBM latency overlaps this frame's FP64 work and flush
+  auto load_frame = [&](int f, float* dst) {
+    const float* fr = a.frames + ((int64_t)s * a.T + f) * P;
+    if (full) {
+      float4 q = __ldcs(reinterpret_cast<const float4*>(fr + pix0));
+      dst[0] = q.x; dst[1] = q.y; dst[2] = q.z; dst[3] = q.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) dst[k] = (pix0 + k < P) ? __ldcs(fr + pix0 + k) : 0.f;
+    }
+  };
+  float vnext[VPT];
+  load_frame(0, vnext);
+  for (int f = 0; f < a.T; ++f) {
+    const int seg = s * a.T + f;
+    int64_t tnow;
+    if (a.t_bounds) {
+      c.tprev = a.t_bounds[(int64_t)s * (a.T + 1) + f];
+      tnow = a.t_bounds[(int64_t)s * (a.T + 1) + f + 1];
+    } else {
+      c.tprev = clock_t0 + (int64_t)f * a.tick;
+      tnow = c.tprev + a.tick;
+    }
+    c.dt = tnow - c.tprev;
+    c.dtd = (double)c.dt;
+    float v[VPT];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) v[k] = vnext[k];
+    if (f + 1 < a.T) load_frame(f + 1, vnext);
+
+    // ---- single pass: lane math, events straight into this lane's smem slots ----
+    float rn[VPT];
+    int64_t ltn[VPT];
+    int tot = 0;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      rn[k] = r[k]; ltn[k] = lt[k];
+      if (pix0 + k < P) {
+        lane_pixel<REFR, UNI>(v[k], r[k], lt[k], thp[k], thn[k], xyk[k], c, s_log, rn[k], ltn[k],
+                              [&](uint64_t key, int) {
+                                if (tot < kSlots) slots[tot * NT + tid] = key;
+                                ++tot;
+                              });
+      }
+    }
+    const bool overflow = __syncthreads_or(tot > kSlots) != 0;
+    {  // chunk reservations: warp ballot, 8 lanes = one 32-pixel chunk
+      const uint32_t m = __ballot_sync(0xffffffffu, tot > 0);
+      if (lane == 0) {
+        const int cc = ((m & 0xffu) != 0) + ((m & 0xff00u) != 0) + ((m & 0xff0000u) != 0) + ((m & 0xff000000u) != 0);
+        if (cc) atomicAdd(&s_res, cc);
+      }
+    }
+    int64_t tile_total;
+    const int64_t excl = block_excl_scan<NT, int64_t>((int64_t)tot, s_scan, &tile_total);
+    const int64_t st_idx = (int64_t)seg * a.ntiles + tile;
+    uint32_t* hr = NB ? a.rows + ((int64_t)seg * a.ngroups + tile / a.gt) * NB : nullptr;
+    if (!overflow) {
+      for (int e = 0; e < tot; ++e) stg[excl + e] = slots[e * NT + tid];
+      __syncthreads();
+      uint64_t* reg = a.region + st_idx * kTileCap;
+      for (int64_t i = tid; i < tile_total; i += NT) {
+        const uint64_t key = stg[i];
+        reg[i] = key;
+        if (NB) atomicAdd(hr + ((uint32_t)(key >> kKeyPixBits) & (uint32_t)(NB - 1)), 1u);
+      }
+      if (tid == 0) { a.tile_count[st_idx] = tile_total; a.tile_ovf[st_idx] = -1; }
+    } else {
+      // a lane exceeded its slots: recompute the tile's events from the
+      // unchanged state straight into the tile region, or, if the whole tile
+      // exceeds its region, into space reserved in the overflow area
+      if (tid == 0) {
+        long long off = -1;
+        if (tile_total > kTileCap) {
+          off = (long long)atomicAdd(a.ovf_cursor + seg, (unsigned long long)tile_total);
+          if (off + tile_total > a.ovf_cap) { a.err[0] = 1; off = -2; }
+        }
+        s_off = off;
+        a.tile_count[st_idx] = tile_total;
+        a.tile_ovf[st_idx] = off;
+      }
+      __syncthreads();
+      const long long off = s_off;
+      if (off >= -1) {
+        uint64_t* dst = off >= 0 ? a.ovf_area + (int64_t)seg * a.ovf_cap + off : a.region + st_idx * kTileCap;
+        int64_t o = excl;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+          if (pix0 + k < P) {
+            float r2;
+            int64_t l2;
+            lane_pixel<REFR, UNI>(v[k], r[k], lt[k], thp[k], thn[k], xyk[k], c, s_log, r2, l2,
+                                  [&](uint64_t key, int) {
+                                    dst[o++] = key;
+                                    if (NB) atomicAdd(hr + ((uint32_t)(key >> kKeyPixBits) & (uint32_t)(NB - 1)), 1u);
+                                  });
+          }
+        }
+      }
+    }
+    if (tid == 0) {
+      if (s_res) atomicAdd(reinterpret_cast<unsigned long long*>(a.seg_res + seg), (unsigned long long)s_res);
+      s_res = 0;
+      if (tile == 0) a.seg_tbase[seg] = c.tprev;
+    }
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      dirty[k] |= (rn[k] != r[k]) || (ltn[k] != lt[k]);
+      r[k] = rn[k];
+      lt[k] = ltn[k];
+    }
+    __syncthreads();  // slots / stg reused by the next frame
+  }
+
+  // ---- state write-back (only pixels whose state changed) ----
+  if (*a.bad != kNoBad) return;  // validation failed: state is not touched
+  if (full && dirty[0] && dirty[1] && dirty[2] && dirty[3]) {
+    *reinterpret_cast<float4*>(refp + pix0) = make_float4(r[0], r[1], r[2], r[3]);
+    *reinterpret_cast<longlong2*>(lastp + pix0) = make_longlong2(lt[0], lt[1]);
+    *reinterpret_cast<longlong2*>(lastp + pix0 + 2) = make_longlong2(lt[2], lt[3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < VPT; ++k)
+      if (dirty[k]) { refp[pix0 + k] = r[k]; lastp[pix0 + k] = lt[k]; }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_tilescan: per segment, pixel-major tile bases (prefix of tile counts),
+// counts / dropped (capacity, parallel.py:261-273), and the column scan of the
+// tile-group t_rel histogram rows (exclusive prefix over groups, bin totals).
+// Block = 32 bins x 16 group chunks.  If the segment exceeds its capacity the
+// rows of the group holding the cut are recounted from its kept keys.
+// ---------------------------------------------------------------------------
+constexpr int kTsBins = 32, kTsChunks = 16, kTsThreads = kTsBins * kTsChunks;
+
+__global__ void __launch_bounds__(kTsThreads) k_tilescan(TileScanArgs a) {
+  __shared__ int64_t s_scan[kTsThreads / 32 + 1];
+  __shared__ int64_t s_run;
+  __shared__ uint32_t s_sum[kTsChunks][kTsBins];
+  __shared__ uint32_t s_fix[kTsBins];
+  const int seg = blockIdx.y, tid = threadIdx.x;
+  const bool bad = *a.bad != kNoBad;
+  const int64_t* cnt = a.tile_count + (int64_t)seg * a.ntiles;
+  // pass 1: total (and tile bases in block 0)
+  if (tid == 0) s_run = 0;
+  __syncthreads();
+  for (int base = 0; base < a.ntiles; base += kTsThreads) {
+    const int q = base + tid;
+    const int64_t v = (q < a.ntiles && !bad) ? cnt[q] : 0;
+    int64_t tt;
+    const int64_t ex = block_excl_scan<kTsThreads, int64_t>(v, s_scan, &tt);
+    if (blockIdx.x == 0 && q < a.ntiles) a.tile_base[(int64_t)seg * a.ntiles + q] = s_run + ex;
+    __syncthreads();
+    if (tid == 0) s_run += tt;
+    __syncthreads();
+  }
+  const int64_t total = s_run;
+  const int64_t written = total < a.cap ? total : a.cap;
+  if (blockIdx.x == 0 && tid == 0 && a.out_count) {
+    a.out_count[seg] = written;
+    a.out_dropped[seg] = (a.err && a.err[0]) ? -1 : total - written;
+  }
+  if (!a.rows) return;
+  const int NB = 1 << a.bits;
+  const int bl = tid % kTsBins, ch = tid / kTsBins;
+  const int d = blockIdx.x * kTsBins + bl;
+  uint32_t* rows = a.rows + (int64_t)seg * a.ngroups * NB;
+  int gcut = a.ngroups;  // groups >= gcut hold no kept event
+  if (total > a.cap) {
+    // rare: find the tile holding the cut (serial scan by one warp is fine here)
+    __shared__ int s_qcut;
+    __shared__ int64_t s_qbase;
+    if (tid == 0) {
+      int64_t run = 0;
+      int q = 0;
+      for (; q < a.ntiles; ++q) {
+        if (run + cnt[q] > a.cap) break;
+        run += cnt[q];
+      }
+      s_qcut = q;
+      s_qbase = run;
+    }
+    if (tid < kTsBins) s_fix[tid] = 0;
+    __syncthreads();
+    const int qcut = s_qcut;
+    const int g = qcut / a.gt;
+    gcut = g + 1;
+    // recount group g's bins [blockIdx.x*32, +32) over its kept keys
+    for (int q = g * a.gt; q <= qcut && q < a.ntiles; ++q) {
+      const int64_t n = (q < qcut) ? cnt[q] : (a.cap - s_qbase);
+      const int64_t ov = a.tile_ovf[(int64_t)seg * a.ntiles + q];
+      const uint64_t* src = ov >= 0 ? a.ovf_area + (int64_t)seg * a.ovf_cap + ov
+                                    : a.region + ((int64_t)seg * a.ntiles + q) * kTileCap;
+      for (int64_t i = tid; i < n; i += kTsThreads) {
+        const int b = (int)((src[i] >> kKeyPixBits) & (uint64_t)(NB - 1));
+        if (b >= blockIdx.x * kTsBins && b < blockIdx.x * kTsBins + kTsBins) atomicAdd(&s_fix[b - blockIdx.x * kTsBins], 1u);
+      }
+    }
+    __syncthreads();
+    if (tid < kTsBins && blockIdx.x * kTsBins + tid < NB) rows[(int64_t)g * NB + blockIdx.x * kTsBins + tid] = s_fix[tid];
+    __syncthreads();
+  }
+  // pass 2: column scan over groups [0, gcut)
+  const int ng = gcut;
+  const int CH = (ng + kTsChunks - 1) / kTsChunks;
+  const int g0 = ch * CH, g1 = min(ng, g0 + CH);
+  uint32_t* col = rows + d;
+  constexpr int kMaxCh = 32;
+  uint32_t cv[kMaxCh];
+  uint32_t sum = 0;
+  if (d < NB && !bad) {
+#pragma unroll
+    for (int u = 0; u < kMaxCh; ++u) cv[u] = (g0 + u < g1) ? col[(int64_t)(g0 + u) * NB] : 0u;
+#pragma unroll
+    for (int u = 0; u < kMaxCh; ++u) sum += cv[u];
+    for (int g = g0 + kMaxCh; g < g1; ++g) sum += col[(int64_t)g * NB];
+  }
+  s_sum[ch][bl] = sum;
+  __syncthreads();
+  uint32_t acc = 0, tot = 0;
+  for (int k = 0; k < kTsChunks; ++k) {
+    const uint32_t v = s_sum[k][bl];
+    if (k < ch) acc += v;
+    tot += v;
+  }
+  if (d < NB && !bad) {
+#pragma unroll
+    for (int u = 0; u < kMaxCh; ++u)
+      if (g0 + u < g1) { col[(int64_t)(g0 + u) * NB] = acc; acc += cv[u]; }
+    for (int g = g0 + kMaxCh; g < g1; ++g) {
+      const uint32_t v = col[(int64_t)g * NB];
+      col[(int64_t)g * NB] = acc;
+      acc += v;
+    }
+  }
+  if (d < NB && ch == 0) a.tot[(int64_t)seg * NB + d] = bad ? 0u : tot;
+}
+
+cudaError_t launch_tilescan(const TileScanArgs& a, cudaStream_t st) {
+  const int NB = a.rows ? (1 << a.bits) : kTsBins;
+  dim3 grid((NB + kTsBins - 1) / kTsBins, a.nseg);
+  k_tilescan<<<grid, kTsThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K2 (tile form): one CTA per (segment, tile group).  Walks the group's tiles
+// in pixel order; each tile's kept keys are ranked by t_rel (warp match-any,
+// per-warp counters: stable) and placed at bin start + earlier-groups prefix +
+// running offset + rank.  pixel_major mode copies the keys to the SoA at the
+// tile base instead (generate_events_serial order).  No inter-CTA waiting.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kOrdThreads) k_tile_order(TileOrderArgs a) {
+  constexpr int NT = kOrdThreads, IPT = kOrdIpt, M = kOrdTile, NW = NT / 32;
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int NB = a.pixel_major ? 1 : (1 << a.bits);
+  uint64_t* sorted = reinterpret_cast<uint64_t*>(sm);
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(sorted + M);  // [NW][NB]
+  uint32_t* lstart = reinterpret_cast<uint32_t*>(wcnt + NW * NB + (NW * NB) % 2);
+  uint32_t* offr = lstart + NB;
+  uint32_t* stot = offr + NB;
+  __shared__ uint32_t s_scan[NW + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int seg = blockIdx.y, g = blockIdx.x;
+  const uint64_t dmask = (uint64_t)(NB - 1);
+  const int per = (NB + NT - 1) / NT;
+  __shared__ const uint64_t* s_gsrc[kMaxGroupTiles];
+  __shared__ int64_t s_gpre[kMaxGroupTiles + 1], s_gtb[kMaxGroupTiles];
+  const int64_t ob = (int64_t)seg * a.seg_stride;
+
+  // group tile table first (independent loads), then the bin offsets
+  const int q0 = g * a.gt;
+  if (tid < a.gt) {
+    const int q = q0 + tid;
+    int64_t nkeep = 0;
+    s_gsrc[tid] = a.region;
+    s_gtb[tid] = 0;
+    if (q < a.ntiles) {
+      const int64_t sq = (int64_t)seg * a.ntiles + q;
+      const int64_t tbase = a.tile_base[sq];
+      const int64_t nq = a.tile_count[sq];
+      nkeep = a.cap - tbase;
+      nkeep = nkeep < 0 ? 0 : (nkeep > nq ? nq : nkeep);
+      const int64_t ov = a.tile_ovf[sq];
+      s_gsrc[tid] = ov >= 0 ? a.ovf_area + (int64_t)seg * a.ovf_cap + ov : a.region + sq * kTileCap;
+      s_gtb[tid] = tbase;
+    }
+    s_gpre[tid + 1] = nkeep;  // counts; prefix below
+  }
+  const bool bad = *a.bad != kNoBad;
+  const int64_t tb0 = a.seg_tbase ? a.seg_tbase[seg] : 0;
+  uint32_t* row = a.pixel_major ? nullptr : a.rows + ((int64_t)seg * a.ngroups + g) * NB;
+  uint32_t tv[8], rv[8];  // NB <= 2048 -> per <= 8
+  if (!a.pixel_major) {
+    for (int j = 0; j < per; ++j) {
+      const int d = tid * per + j;
+      tv[j] = d < NB ? a.tot[(int64_t)seg * NB + d] : 0u;
+      rv[j] = d < NB ? row[d] : 0u;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    s_gpre[0] = 0;
+    for (int j = 0; j < a.gt; ++j) s_gpre[j + 1] += s_gpre[j];
+  }
+  if (!a.pixel_major) {
+    uint32_t sum = 0;
+    for (int j = 0; j < per; ++j) sum += tv[j];
+    uint32_t tt;
+    uint32_t ex = block_excl_scan<NT, uint32_t>(sum, s_scan, &tt);  // (syncs)
+    for (int j = 0; j < per; ++j) {
+      const int d = tid * per + j;
+      if (d < NB) {
+        offr[d] = ex + rv[j];
+        row[d] = 0;  // rows are accumulated with atomics by the next step's K1
+        ex += tv[j];
+      }
+    }
+  }
+  __syncthreads();
+  if (bad) return;
+  const int64_t ng = s_gpre[a.gt];
+
+  if (a.pixel_major) {
+    for (int j = 0; j < a.gt; ++j) {
+      const uint64_t* src = s_gsrc[j];
+      const int64_t n = s_gpre[j + 1] - s_gpre[j], tb = s_gtb[j];
+      for (int64_t i = tid; i < n; i += NT) {
+        const uint64_t k = __ldcs(src + i);
+        const int64_t gp = ob + tb + i;
+        a.out_t[gp] = tb0 + (int64_t)(k >> kKeyPixBits);
+        a.out_x[gp] = (uint16_t)((k >> 1) & 0xffffu);
+        a.out_y[gp] = (uint16_t)((k >> 17) & 0xffffu);
+        a.out_p[gp] = (k & 1u) ? (int8_t)1 : (int8_t)-1;
+      }
+    }
+    return;
+  }
+  {
+    for (int64_t base = 0; base < ng; base += M) {
+      const int cnt = (int)((ng - base) < M ? (ng - base) : M);
+      for (int d = lane; d < NB; d += 32) wcnt[warp * NB + d] = 0;
+      __syncwarp();
+      uint64_t key[IPT];
+      uint32_t rank[IPT];
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) {
+        const int idx = warp * 32 * IPT + k * 32 + lane;
+        key[k] = 0ull;
+        if (idx < cnt) {
+          const int64_t gi = base + idx;
+          int j = 0;  // last tile with gpre[j] <= gi (binary search over <= 16 tiles)
+          for (int step = kMaxGroupTiles / 2; step > 0; step >>= 1)
+            if (j + step < a.gt && s_gpre[j + step] <= gi) j += step;
+          key[k] = __ldcs(s_gsrc[j] + (gi - s_gpre[j]));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) {
+        const int idx = warp * 32 * IPT + k * 32 + lane;
+        const bool valid = idx < cnt;
+        const int d = valid ? (int)((key[k] >> a.shift) & dmask) : NB;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (valid && lane == leader) {
+          old = wcnt[warp * NB + d];
+          wcnt[warp * NB + d] = (uint16_t)(old + __popc(peers));
+        }
+        old = __shfl_sync(0xffffffffu, old, leader);
+        rank[k] = old + __popc(peers & lanemask_lt());
+        __syncwarp();
+      }
+      __syncthreads();
+      for (int d = tid; d < NB; d += NT) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int w2 = 0; w2 < NW; ++w2) {
+          const uint32_t cc = wcnt[w2 * NB + d];
+          wcnt[w2 * NB + d] = (uint16_t)acc;
+          acc += cc;
+        }
+        stot[d] = acc;
+      }
+      __syncthreads();
+      {
+        uint32_t sum = 0;
+        for (int j = 0; j < per; ++j) { const int d = tid * per + j; if (d < NB) sum += stot[d]; }
+        uint32_t tt;
+        uint32_t ex = block_excl_scan<NT, uint32_t>(sum, s_scan, &tt);
+        for (int j = 0; j < per; ++j) { const int d = tid * per + j; if (d < NB) { lstart[d] = ex; ex += stot[d]; } }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) {
+        const int idx = warp * 32 * IPT + k * 32 + lane;
+        if (idx < cnt) {
+          const int d = (int)((key[k] >> a.shift) & dmask);
+          sorted[lstart[d] + wcnt[warp * NB + d] + rank[k]] = key[k];
+        }
+      }
+      __syncthreads();
+      if (a.final_soa) {
+        for (int i = tid; i < cnt; i += NT) {
+          const uint64_t k = sorted[i];
+          const int d = (int)((k >> a.shift) & dmask);
+          const int64_t gp = ob + (int64_t)(offr[d] + (uint32_t)i - lstart[d]);
+          a.out_t[gp] = tb0 + (int64_t)(k >> kKeyPixBits);
+          a.out_x[gp] = (uint16_t)((k >> 1) & 0xffffu);
+          a.out_y[gp] = (uint16_t)((k >> 17) & 0xffffu);
+          a.out_p[gp] = (k & 1u) ? (int8_t)1 : (int8_t)-1;
+        }
+      } else {
+        for (int i = tid; i < cnt; i += NT) {
+          const uint64_t k = sorted[i];
+          const int d = (int)((k >> a.shift) & dmask);
+          a.keys_out[ob + (int64_t)(offr[d] + (uint32_t)i - lstart[d])] = k;
+        }
+      }
+      __syncthreads();
+      for (int d = tid; d < NB; d += NT) offr[d] += stot[d];
+      __syncthreads();
+    }
+  }
+}
+
+cudaError_t launch_tile_order(const TileOrderArgs& a, cudaStream_t st) {
+  const int NB = a.pixel_major ? 1 : (1 << a.bits);
+  const size_t smem = (size_t)kOrdTile * 8 + (size_t)(kOrdThreads / 32) * NB * 2 + 4 + (size_t)NB * 12;
+  ensure_smem_gen(k_tile_order);
+  dim3 grid(a.ngroups, a.nseg);
+  k_tile_order<<<grid, kOrdThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <bool VEC, bool REFR, bool UNI>
+static cudaError_t gen_dispatch(const GenArgs& a, unsigned grid, size_t smem, cudaStream_t st) {
+  auto k = k_generate<VEC, REFR, UNI>;
+  ensure_smem_gen(k);
+  k<<<grid, kGenThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_generate(const GenArgs& a0, int uniform_th, cudaStream_t st) {
+  GenArgs a = a0;
+  a.rth_pos = 1.0 / (double)a.thp_u;  // IEEE reciprocals of the uniform thresholds
+  a.rth_neg = 1.0 / (double)a.thn_u;
+  const unsigned grid = (unsigned)((int64_t)a.S * a.ntiles);
+  const size_t smem = (size_t)kSlots * kGenThreads * 8 + (size_t)kTileCap * 8;
+  const bool vec = (a.P % 4 == 0) && ((uintptr_t)a.frames % 16 == 0) && ((uintptr_t)a.ref % 16 == 0) &&
+                   ((uintptr_t)a.last % 16 == 0) &&
+                   (uniform_th || (((uintptr_t)a.thp % 16 == 0) && ((uintptr_t)a.thn % 16 == 0)));
+  const bool refr = a.refr > 0;
+  if (vec) {
+    if (refr) return uniform_th ? gen_dispatch<true, true, true>(a, grid, smem, st)
+                                : gen_dispatch<true, true, false>(a, grid, smem, st);
+    return uniform_th ? gen_dispatch<true, false, true>(a, grid, smem, st)
+                      : gen_dispatch<true, false, false>(a, grid, smem, st);
+  }
+  if (refr) return uniform_th ? gen_dispatch<false, true, true>(a, grid, smem, st)
+                              : gen_dispatch<false, true, false>(a, grid, smem, st);
+  return uniform_th ? gen_dispatch<false, false, true>(a, grid, smem, st)
+                    : gen_dispatch<false, false, false>(a, grid, smem, st);
+}
+
+}  // namespace evs

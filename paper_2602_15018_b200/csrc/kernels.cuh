@@ -64,9 +64,67 @@ struct GenArgs {
   int ngroups;
   float log_eps_f;  // log_eps rounded to f32 (prefilter only)
   double rth_pos, rth_neg;  // 1/th for uniform thresholds (set by launch_generate)
+  // per-tile event regions (no inter-tile dependency in K1):
+  uint64_t* region;          // [nseg][ntiles][kTileCap] pixel-major keys
+  int64_t* tile_count;       // [nseg][ntiles] events of the tile (before capacity)
+  int64_t* tile_ovf;         // [nseg][ntiles] -1, or offset into ovf_area (lane slot overflow)
+  uint64_t* ovf_area;        // [nseg][ovf_cap]
+  unsigned long long* ovf_cursor;  // [nseg], zeroed by the prologue
+  int64_t ovf_cap;
+  int64_t* err;              // [1] != 0: overflow area exhausted
+  int gt;                    // tiles per group (histogram row)
 };
 
-constexpr int kGroupTiles = 4;  // K1 tiles per histogram row / per K2 CTA
+constexpr int kSlotsPerLane = 16;
+constexpr int kTileCap = kSlotsPerLane * kGenThreads;  // keys per tile region
+
+struct TileScanArgs {
+  int nseg, ntiles, ngroups, bits;
+  int64_t cap;
+  const int64_t* tile_count;  // [nseg][ntiles]
+  const int64_t* tile_ovf;
+  const uint64_t* region;
+  const uint64_t* ovf_area;
+  int64_t ovf_cap;
+  int64_t* tile_base;         // out [nseg][ntiles] pixel-major base of each tile
+  uint32_t* rows;             // [nseg][ngroups][NB] (null: counts only)
+  uint32_t* tot;              // out [nseg][NB]
+  int64_t* out_count;
+  int64_t* out_dropped;
+  const int64_t* bad;
+  const int64_t* err;         // K1 overflow-area exhaustion -> out_dropped = -1
+  int gt;
+};
+
+struct TileOrderArgs {
+  int nseg, ntiles, ngroups, bits, shift;
+  int64_t cap;
+  const int64_t* tile_count;
+  const int64_t* tile_ovf;
+  const int64_t* tile_base;
+  const uint64_t* region;
+  const uint64_t* ovf_area;
+  int64_t ovf_cap;
+  uint32_t* rows;
+  const uint32_t* tot;
+  int64_t seg_stride;         // output stride per segment
+  int final_soa;              // 1: SoA out; 0: keys_out
+  int pixel_major;            // 1: plain compaction (serial order), no t ordering
+  uint64_t* keys_out;
+  int64_t* out_t;
+  uint16_t* out_x;
+  uint16_t* out_y;
+  int8_t* out_p;
+  const int64_t* seg_tbase;
+  const int64_t* bad;
+  int gt;
+};
+
+cudaError_t launch_tilescan(const TileScanArgs& a, cudaStream_t st);
+cudaError_t launch_tile_order(const TileOrderArgs& a, cudaStream_t st);
+
+constexpr int kGroupTiles = 4;      // legacy group size (generic path)
+constexpr int kMaxGroupTiles = 16;  // K1 tiles per histogram row / per K2 CTA (runtime gt <= this)
 
 struct ColScanArgs {
   int nseg, ngroups, bits;
@@ -145,7 +203,7 @@ struct HistArgs {
 // host launchers (kernels.cu)
 cudaError_t launch_prologue(const float* frames, int64_t nframes, int64_t P, int validate,
                             int64_t* bad, int64_t* seg_res, int nseg, StepDesc* desc,
-                            int64_t t_advance, cudaStream_t st);
+                            int64_t t_advance, int64_t* zero2, int64_t n2, cudaStream_t st);
 cudaError_t launch_generate(const GenArgs& a, int uniform_th, cudaStream_t st);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t st);
 cudaError_t launch_hist(const HistArgs& a, cudaStream_t st);

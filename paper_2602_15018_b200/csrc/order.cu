@@ -25,9 +25,11 @@ namespace evs {
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_prologue(const float* __restrict__ frames, int64_t n,
                                                   int validate, int64_t* bad, int64_t* seg_res,
-                                                  int nseg, StepDesc* desc, int64_t t_advance) {
+                                                  int nseg, StepDesc* desc, int64_t t_advance,
+                                                  int64_t* zero2, int64_t n2) {
   if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < nseg; i += blockDim.x) seg_res[i] = 0;
+    for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) zero2[i] = 0;
     if (desc && threadIdx.x == 0) {  // advance the device clock for this step
       desc->cur_t0 = desc->next_t0;
       desc->next_t0 += t_advance;
@@ -67,7 +69,7 @@ __global__ void __launch_bounds__(256) k_prologue(const float* __restrict__ fram
 
 cudaError_t launch_prologue(const float* frames, int64_t nframes_px, int64_t P, int validate,
                             int64_t* bad, int64_t* seg_res, int nseg, StepDesc* desc,
-                            int64_t t_advance, cudaStream_t st) {
+                            int64_t t_advance, int64_t* zero2, int64_t n2, cudaStream_t st) {
   (void)P;
   int64_t work = validate ? (nframes_px + 3) / 4 : 1;
   int64_t blocks = (work + 255) / 256;
@@ -76,10 +78,10 @@ cudaError_t launch_prologue(const float* frames, int64_t nframes_px, int64_t P, 
   bool vec = ((uintptr_t)frames % 16) == 0;
   if (vec)
     k_prologue<true><<<(unsigned)blocks, 256, 0, st>>>(frames, nframes_px, validate, bad, seg_res, nseg,
-                                                       desc, t_advance);
+                                                       desc, t_advance, zero2, n2);
   else
     k_prologue<false><<<(unsigned)blocks, 256, 0, st>>>(frames, nframes_px, validate, bad, seg_res, nseg,
-                                                        desc, t_advance);
+                                                        desc, t_advance, zero2, n2);
   return cudaGetLastError();
 }
 

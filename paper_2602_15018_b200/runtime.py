@@ -178,6 +178,9 @@ class StepEngine:
 
         host = torch.cat([self.info.reshape(-1), self.bad]).cpu().numpy()
         nseg = self.info.shape[1]
+        if int(host[-1]) == _lib.NO_BAD and (host[nseg:2 * nseg] < 0).any():
+            raise _lib.NativeError("event overflow area exhausted (a frame far above its capacity "
+                                   "concentrated > 4 events/pixel in many tiles); raise max_events_per_frame")
         return host[:nseg], host[nseg:2 * nseg], host[2 * nseg:3 * nseg], int(host[-1])
 
     def reset_bad(self) -> None:
