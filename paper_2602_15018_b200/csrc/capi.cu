@@ -35,6 +35,7 @@ int sm_count_current() {
 struct StepLayout {
   int nseg, ntiles, npass, bits, NB, ngroups, gt;
   int64_t max_tiles2, ovf_cap;
+  size_t chunk_flag;
   size_t ctr, desc, zero2, region, tile_count, tile_ovf, tile_base, ovf_area, rows, tot, hist, gstart,
       seg_tbase, seg_tile_prefix, status2, keysA, keysB, total;
 };
@@ -79,6 +80,7 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   L->ctr = off; off = align_up(off + 64 * sizeof(uint32_t));
   L->desc = off; off = align_up(off + sizeof(StepDesc));
   L->zero2 = off; off = align_up(off + (ns + 1) * 8);  // ovf_cursor[nseg] + err
+  L->chunk_flag = off; off = align_up(off + (size_t)p->streams * nt * 8);
   L->tile_count = off; off = align_up(off + ns * nt * 8);
   L->tile_ovf = off; off = align_up(off + ns * nt * 8);
   L->tile_base = off; off = align_up(off + ns * nt * 8);
@@ -172,6 +174,19 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   g.rows = canon ? at<uint32_t>(ws, L.rows) : nullptr;
   g.ngroups = L.ngroups;
   g.gt = L.gt;
+  {
+    // split each tile's T frames into chunks so the grid is >= ~8 waves of
+    // resident K1 CTAs (3 per SM): the tail wave then lasts one short chunk
+    const int64_t resident = (int64_t)sm_count_current() * 3;
+    const int64_t tiles = (int64_t)p->streams * L.ntiles;
+    int64_t nch = (8 * resident + tiles - 1) / tiles;
+    if (nch > p->frames) nch = p->frames;
+    if (nch > 255) nch = 255;
+    if (nch < 1) nch = 1;
+    g.tc = (int)((p->frames + nch - 1) / nch);
+    g.nchunks = (p->frames + g.tc - 1) / g.tc;
+    g.chunk_flag = at<unsigned long long>(ws, L.chunk_flag);
+  }
   g.region = at<uint64_t>(ws, L.region);
   g.tile_count = at<int64_t>(ws, L.tile_count);
   g.tile_ovf = at<int64_t>(ws, L.tile_ovf);

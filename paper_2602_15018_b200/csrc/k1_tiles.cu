@@ -150,12 +150,18 @@ __device__ __forceinline__ int lane_pixel(float v, float r, int64_t lt, float th
   // t_rel(j) = int(((j*th)/|diff|)*dt) (model.py:144): j * u, exact fallback
   // whenever the floor of the approximation could differ from the reference's
   const double u = thd * rcp_nr(ad) * c.dtd;
+  // j*u is within ~8e-16 relative of the reference's RN(RN(j*th/|diff|)*dt);
+  // a loop-invariant band of 4e-15 * n*u around every integer triggers the
+  // exact IEEE evaluation (never in practice except on designed boundaries)
+  const double lim = 0.5 - ((double)n * u * 4e-15 + 1e-290);
   const uint64_t xyp = xy | (pos ? 1u : 0u);
   int kept = 0;
   int64_t l = lt;
   for (int j = 1; j <= n; ++j) {
-    int64_t tr = safe_floor((double)j * u);
-    if (tr < 0) tr = (int64_t)((((double)j * thd) / ad) * c.dtd);
+    const double y = (double)j * u;
+    const double fl = floor(y);
+    int64_t tr = (int64_t)fl;
+    if (fabs((y - fl) - 0.5) > lim) tr = (int64_t)((((double)j * thd) / ad) * c.dtd);
     if (tr > c.dt - 1) tr = c.dt - 1;  // model.py:145-146
     if (REFR) {
       if (c.tprev + tr - l < c.refr) continue;  // model.py:148-149
@@ -219,13 +225,33 @@ __global__ void __launch_bounds__(kGenThreads, 3) k_generate(GenArgs a) {
   __shared__ int s_res;
 
   const int tid = threadIdx.x, lane = tid & 31;
-  const int s = (int)(blockIdx.x / (uint32_t)a.ntiles);
-  const int tile = (int)(blockIdx.x % (uint32_t)a.ntiles);
+  const uint32_t st_tiles = (uint32_t)a.S * (uint32_t)a.ntiles;
+  const int chunk = (int)(blockIdx.x / st_tiles);
+  const uint32_t stile = blockIdx.x % st_tiles;
+  const int s = (int)(stile / (uint32_t)a.ntiles);
+  const int tile = (int)(stile % (uint32_t)a.ntiles);
+  const int f_begin = chunk * a.tc;
+  const int f_end = min(a.T, f_begin + a.tc);
   const int64_t P = a.P;
   const int64_t pix0 = (int64_t)tile * TILE + (int64_t)tid * VPT;
   const bool full = VEC && (pix0 + VPT <= P);
   float* refp = a.ref + (int64_t)s * P;
   int64_t* lastp = a.last + (int64_t)s * P;
+  const uint32_t epoch = a.desc ? a.desc->cur_epoch : a.epoch;
+  if (chunk > 0) {
+    // wait for the previous frame chunk of this tile (a lower block index, so
+    // already resident or finished), then read the state it left in HBM
+    if (tid == 0) {
+      const unsigned long long want = ((unsigned long long)epoch << 8) | (unsigned long long)chunk;
+      unsigned long long v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.chunk_flag + stile) : "memory");
+        if (v == want) break;
+        __nanosleep(256);
+      }
+    }
+    __syncthreads();
+  }
 
   float r[VPT], thp[VPT], thn[VPT];
   int64_t lt[VPT];
@@ -233,11 +259,11 @@ __global__ void __launch_bounds__(kGenThreads, 3) k_generate(GenArgs a) {
 #pragma unroll
   for (int k = 0; k < VPT; ++k) { r[k] = 0.f; lt[k] = 0; dirty[k] = false; thp[k] = a.thp_u; thn[k] = a.thn_u; }
   if (full) {
-    float4 q = *reinterpret_cast<const float4*>(refp + pix0);
+    float4 q = __ldcg(reinterpret_cast<const float4*>(refp + pix0));
     r[0] = q.x; r[1] = q.y; r[2] = q.z; r[3] = q.w;
     if (REFR) {
-      longlong2 l0 = *reinterpret_cast<const longlong2*>(lastp + pix0);
-      longlong2 l1 = *reinterpret_cast<const longlong2*>(lastp + pix0 + 2);
+      longlong2 l0 = __ldcg(reinterpret_cast<const longlong2*>(lastp + pix0));
+      longlong2 l1 = __ldcg(reinterpret_cast<const longlong2*>(lastp + pix0 + 2));
       lt[0] = l0.x; lt[1] = l0.y; lt[2] = l1.x; lt[3] = l1.y;
     }
     if (!UNI) {
@@ -250,8 +276,8 @@ __global__ void __launch_bounds__(kGenThreads, 3) k_generate(GenArgs a) {
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
       if (pix0 + k < P) {
-        r[k] = refp[pix0 + k];
-        if (REFR) lt[k] = lastp[pix0 + k];
+        r[k] = __ldcg(refp + pix0 + k);
+        if (REFR) lt[k] = __ldcg(lastp + pix0 + k);
         if (!UNI) { thp[k] = a.thp[(int64_t)s * P + pix0 + k]; thn[k] = a.thn[(int64_t)s * P + pix0 + k]; }
       }
     }
@@ -295,8 +321,8 @@ __global__ void __launch_bounds__(kGenThreads, 3) k_generate(GenArgs a) {
     }
   };
   float vnext[VPT];
-  load_frame(0, vnext);
-  for (int f = 0; f < a.T; ++f) {
+  load_frame(f_begin, vnext);
+  for (int f = f_begin; f < f_end; ++f) {
     const int seg = s * a.T + f;
     int64_t tnow;
     if (a.t_bounds) {
@@ -311,7 +337,7 @@ __global__ void __launch_bounds__(kGenThreads, 3) k_generate(GenArgs a) {
     float v[VPT];
 #pragma unroll
     for (int k = 0; k < VPT; ++k) v[k] = vnext[k];
-    if (f + 1 < a.T) load_frame(f + 1, vnext);
+    if (f + 1 < f_end) load_frame(f + 1, vnext);
 
     // ---- single pass: lane math, events straight into this lane's smem slots ----
     float rn[VPT];
@@ -398,15 +424,25 @@ __global__ void __launch_bounds__(kGenThreads, 3) k_generate(GenArgs a) {
   }
 
   // ---- state write-back (only pixels whose state changed) ----
-  if (*a.bad != kNoBad) return;  // validation failed: state is not touched
-  if (full && dirty[0] && dirty[1] && dirty[2] && dirty[3]) {
-    *reinterpret_cast<float4*>(refp + pix0) = make_float4(r[0], r[1], r[2], r[3]);
-    *reinterpret_cast<longlong2*>(lastp + pix0) = make_longlong2(lt[0], lt[1]);
-    *reinterpret_cast<longlong2*>(lastp + pix0 + 2) = make_longlong2(lt[2], lt[3]);
-  } else {
+  if (*a.bad == kNoBad) {  // validation failed: state is not touched
+    if (full && dirty[0] && dirty[1] && dirty[2] && dirty[3]) {
+      *reinterpret_cast<float4*>(refp + pix0) = make_float4(r[0], r[1], r[2], r[3]);
+      *reinterpret_cast<longlong2*>(lastp + pix0) = make_longlong2(lt[0], lt[1]);
+      *reinterpret_cast<longlong2*>(lastp + pix0 + 2) = make_longlong2(lt[2], lt[3]);
+    } else {
 #pragma unroll
-    for (int k = 0; k < VPT; ++k)
-      if (dirty[k]) { refp[pix0 + k] = r[k]; lastp[pix0 + k] = lt[k]; }
+      for (int k = 0; k < VPT; ++k)
+        if (dirty[k]) { refp[pix0 + k] = r[k]; lastp[pix0 + k] = lt[k]; }
+    }
+  }
+  if (a.nchunks > 1 && chunk + 1 < a.nchunks) {
+    // hand the tile's state to the next frame chunk (release after all writes)
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned long long v = ((unsigned long long)epoch << 8) | (unsigned long long)(chunk + 1);
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.chunk_flag + stile), "l"(v) : "memory");
+    }
   }
 }
 
@@ -629,15 +665,20 @@ __global__ void __launch_bounds__(kOrdThreads) k_tile_order(TileOrderArgs a) {
       __syncwarp();
       uint64_t key[IPT];
       uint32_t rank[IPT];
+      // tile of the warp's first key (uniform search), then monotone per key
+      int jw = 0;
+      {
+        const int64_t gi0 = base + warp * 32 * IPT;
+        while (jw + 1 < a.gt && s_gpre[jw + 1] <= gi0) ++jw;
+      }
 #pragma unroll
       for (int k = 0; k < IPT; ++k) {
         const int idx = warp * 32 * IPT + k * 32 + lane;
         key[k] = 0ull;
         if (idx < cnt) {
           const int64_t gi = base + idx;
-          int j = 0;  // last tile with gpre[j] <= gi (binary search over <= 16 tiles)
-          for (int step = kMaxGroupTiles / 2; step > 0; step >>= 1)
-            if (j + step < a.gt && s_gpre[j + step] <= gi) j += step;
+          int j = jw;
+          while (j + 1 < a.gt && s_gpre[j + 1] <= gi) ++j;
           key[k] = __ldcs(s_gsrc[j] + (gi - s_gpre[j]));
         }
       }
@@ -731,7 +772,7 @@ cudaError_t launch_generate(const GenArgs& a0, int uniform_th, cudaStream_t st) 
   GenArgs a = a0;
   a.rth_pos = 1.0 / (double)a.thp_u;  // IEEE reciprocals of the uniform thresholds
   a.rth_neg = 1.0 / (double)a.thn_u;
-  const unsigned grid = (unsigned)((int64_t)a.S * a.ntiles);
+  const unsigned grid = (unsigned)((int64_t)a.S * a.ntiles * (a.nchunks > 0 ? a.nchunks : 1));
   const size_t smem = (size_t)kSlots * kGenThreads * 8 + (size_t)kTileCap * 8;
   const bool vec = (a.P % 4 == 0) && ((uintptr_t)a.frames % 16 == 0) && ((uintptr_t)a.ref % 16 == 0) &&
                    ((uintptr_t)a.last % 16 == 0) &&

@@ -73,6 +73,11 @@ struct GenArgs {
   int64_t ovf_cap;
   int64_t* err;              // [1] != 0: overflow area exhausted
   int gt;                    // tiles per group (histogram row)
+  // frame chunking: block b handles chunk c = b / (S*ntiles) = frames
+  // [c*tc, min(T, (c+1)*tc)) of its tile; chunk c waits for chunk c-1 of the
+  // same tile through chunk_flag[(s, tile)] = (launch << 8) | chunks_done
+  int nchunks, tc;
+  unsigned long long* chunk_flag;  // [S*ntiles]
 };
 
 constexpr int kSlotsPerLane = 16;
