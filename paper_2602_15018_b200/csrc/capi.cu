@@ -8,11 +8,13 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/evsim_b200.h"
 #include "common.cuh"
 #include "kernels.cuh"
+#include "fast_path.cuh"
 
 using namespace evs;
 
@@ -38,7 +40,36 @@ struct StepLayout {
   size_t chunk_flag;
   size_t ctr, desc, zero2, region, tile_count, tile_ovf, tile_base, ovf_area, rows, tot, hist, gstart,
       seg_tbase, seg_tile_prefix, status2, keysA, keysB, total;
+  // fast canonical path (fast_path.cu)
+  bool fast;
+  int fG, fntiles, fnbk;
+  size_t fkeys, frows, fsrc, fsnapr, fsnapl, fareau, fareas, fitems, flim, fredon;
 };
+
+// Fast path: canonical order, t_now - t_prev <= 2048 us, P < 2^24.  Tiles of
+// G <= 2048 pixels (a multiple of 32, so tiles start on 32-pixel chunk
+// boundaries) sized so the S*ntiles CTAs fill whole waves of 2 CTAs per SM.
+bool fast_shape(const evs_step_params* p, int64_t P, int64_t mdt, int* G, int* ntiles, int* nbk) {
+  if (p->order != EVS_ORDER_CANONICAL || mdt < 1 || mdt > 8 * kFMaxBuckets) return false;
+  const char* force = getenv("EVS_FORCE_LEGACY");
+  if (force && force[0] == '1') return false;
+  if (P >= (1ll << 24) || (int64_t)p->frames * mdt >= (1ll << 29)) return false;
+  if (p->refractory_us >= (1ll << 29)) return false;
+  const int64_t slots = 2ll * sm_count_current();
+  const int64_t S = p->streams;
+  const int64_t min_tiles = (P + kFGmax - 1) / kFGmax;
+  const int64_t waves = (S * min_tiles + slots - 1) / slots;
+  int64_t nt = (waves * slots + S - 1) / S;
+  int64_t g = (P + nt - 1) / nt;
+  g = (g + 31) / 32 * 32;
+  if (g > kFGmax) g = kFGmax;
+  nt = (P + g - 1) / g;
+  if (nt > kFMaxTiles) return false;
+  *G = (int)g;
+  *ntiles = (int)nt;
+  *nbk = (int)((mdt + 7) / 8);
+  return true;
+}
 
 __global__ void k_clock_init(StepDesc* d, int64_t t0, uint32_t epoch) {
   d->next_t0 = t0;
@@ -93,8 +124,25 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   L->status2 = off; off = align_up(off + ns * L->max_tiles2 * L->NB * 8);
   L->keysA = off; off = align_up(off + (canon && L->npass > 1 ? ns * p->capacity * 8 : 0));
   L->keysB = off; off = align_up(off + (canon && L->npass > 1 ? ns * p->capacity * 8 : 0));
-  L->region = off; off = align_up(off + ns * nt * kTileCap * 8);
-  L->ovf_area = off; off = align_up(off + ns * (size_t)L->ovf_cap * 8);
+  const bool fast_sel = fast_shape(p, P, canon ? (p->max_dt > 0 ? p->max_dt : p->tick) : 0, &L->fG,
+                                   &L->fntiles, &L->fnbk);
+  L->region = off; off = align_up(off + (fast_sel ? 0 : ns * nt * kTileCap * 8));
+  L->ovf_area = off; off = align_up(off + (fast_sel ? 0 : ns * (size_t)L->ovf_cap * 8));
+  L->fast = fast_shape(p, P, canon ? (p->max_dt > 0 ? p->max_dt : p->tick) : 0, &L->fG, &L->fntiles, &L->fnbk);
+  if (L->fast) {
+    const size_t fnt = (size_t)L->fntiles;
+    const size_t cap = (size_t)(p->capacity > 0 ? p->capacity : 1);
+    L->fkeys = off; off = align_up(off + ns * fnt * kFListCap * 4);
+    L->frows = off; off = align_up(off + ns * (L->fnbk + 1) * fnt * 4);
+    L->fsrc = off; off = align_up(off + ns * fnt * 8);
+    L->fsnapr = off; off = align_up(off + ns * fnt * L->fG * 4);
+    L->fsnapl = off; off = align_up(off + ns * fnt * L->fG * 4);
+    L->fareau = off; off = align_up(off + ns * cap * 4);
+    L->fareas = off; off = align_up(off + ns * cap * 4);
+    L->fitems = off; off = align_up(off + ns * fnt * 8);
+    L->flim = off; off = align_up(off + ns * fnt * 4);
+    L->fredon = off; off = align_up(off + ns * 4);
+  }
   L->total = off;
   return true;
 }
@@ -155,6 +203,40 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
                                   L.nseg + 1, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(1);
+
+  if (L.fast) {
+    FastArgs fa;
+    memset(&fa, 0, sizeof(fa));
+    fa.S = p->streams; fa.T = p->frames; fa.W = p->width; fa.P = P;
+    fa.G = L.fG; fa.ntiles = L.fntiles; fa.nbk = L.fnbk;
+    fa.vec = (P % 4 == 0) && ((uintptr_t)b->frames % 16 == 0) && ((uintptr_t)b->ref_log % 16 == 0) &&
+             ((uintptr_t)b->last_event_t % 16 == 0) &&
+             (b->th_pos == nullptr || (((uintptr_t)b->th_pos % 16 == 0) && ((uintptr_t)b->th_neg % 16 == 0)));
+    fa.log_eps = p->log_eps; fa.log_eps_f = (float)p->log_eps;
+    fa.refr = (int)p->refractory_us;
+    fa.thp_u = p->th_pos_uniform; fa.thn_u = p->th_neg_uniform;
+    fa.rthp_u = (float)(1.0 / (double)p->th_pos_uniform);
+    fa.rthn_u = (float)(1.0 / (double)p->th_neg_uniform);
+    fa.frames = b->frames; fa.t_bounds = b->t_bounds; fa.t0 = p->t0; fa.tick = p->tick; fa.desc = desc;
+    fa.ref = b->ref_log; fa.last = b->last_event_t; fa.thp = b->th_pos; fa.thn = b->th_neg;
+    fa.bad = b->bad_pixel; fa.seg_res = b->reservations;
+    fa.keys = at<uint32_t>(ws, L.fkeys); fa.rows = at<uint32_t>(ws, L.frows);
+    fa.tile_src = at<int64_t>(ws, L.fsrc);
+    fa.snap_ref = at<float>(ws, L.fsnapr); fa.snap_last = at<int>(ws, L.fsnapl);
+    fa.area_unsorted = at<uint32_t>(ws, L.fareau); fa.area_sorted = at<uint32_t>(ws, L.fareas);
+    fa.redo_items = at<int>(ws, L.fitems); fa.redo_lim = at<int>(ws, L.flim); fa.redo_n = at<int>(ws, L.fredon);
+    fa.cap = p->capacity; fa.out_count = b->counts; fa.out_dropped = b->dropped;
+    fa.seg_stride = p->capacity;
+    fa.out_t = b->ev_t; fa.out_x = b->ev_x; fa.out_y = b->ev_y; fa.out_p = b->ev_p;
+    if (launch_fast_gen(fa, st) != cudaSuccess) return EVS_ERR_CUDA;
+    mark(2);
+    if (launch_fast_fix(fa, L.nseg, st) != cudaSuccess) return EVS_ERR_CUDA;
+    if (launch_fast_redo(fa, L.nseg, st) != cudaSuccess) return EVS_ERR_CUDA;
+    mark(3);
+    if (launch_fast_order(fa, L.nseg, st) != cudaSuccess) return EVS_ERR_CUDA;
+    mark(4);
+    return EVS_OK;
+  }
 
   GenArgs g;
   memset(&g, 0, sizeof(g));

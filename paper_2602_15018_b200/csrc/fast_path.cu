@@ -1,0 +1,960 @@
+// Fast canonical-order path of evs_step for sm_100a (t_now - t_prev <= 2048 us,
+// the reference's render-rate regime: ticks of 1000 us in every BASELINE config).
+//
+//   k_fast_gen   (K1) one CTA per tile of G <= 2048 consecutive pixels of one
+//                stream, all T frames of the call with the state in registers.
+//                Per frame: certified f32 lane math (exact FP64 fallback),
+//                block-scan compaction of the crossings into a pixel-major
+//                smem list, stable bucket sort of the list in smem (warp
+//                match-any ranks, buckets of 8 t_rel bins), coalesced write of
+//                the sorted 4-byte keys to the tile's slot and of the tile's
+//                bucket starts into a [bucket][tile] table.
+//   k_fast_fix   per segment: counts / dropped (parallel.py:261-273), sorting of
+//                tiles whose crossings overflowed the smem list, and the
+//                capacity cut (first `cap` events in pixel-major order are kept,
+//                model.py:150-158).  Exits at once in the common case.
+//   k_fast_order (K2) one CTA per (segment, bucket): gathers the bucket's slice
+//                of every tile (tile order = pixel order), stable counting sort
+//                by t_rel within the bucket, and writes its contiguous range of
+//                the canonical (t, y, x, p) output with coalesced stores.
+//
+// Lane math (model.py:124-163 / parallel.py:152-217).  The reference computes
+// ln in f64, the crossing count floor(|d|/th + 1e-4) and the times
+// floor(((j*th)/|d|)*dt) in f64.  Every observable (n, t_rel, the refractory
+// filter, the new level f32(ls +- n*th)) depends on |d| only through those
+// floors, so K1 evaluates them in f32 from a "lite" log (table + f32 log1p,
+// |error| < 4e-9) and certifies each floor with an error band; a pixel whose
+// band straddles an integer (about 1e-3 of the events) is recomputed with the
+// exact path (<= 1 ulp f64 log and IEEE division, the formulas of the
+// reference).  The new level is always computed in f64 from the certified n.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/evsim_b200.h"
+#include "common.cuh"
+#include "fast_path.cuh"
+#include "log_table.h"
+
+namespace evs {
+
+// ---------------------------------------------------------------------------
+// exact lane math (rare path): the reference's formulas with a <= 1 ulp log
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void two_sum_x(double a, double b, double& s, double& e) {
+  s = a + b;
+  const double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
+}
+
+// log(x), <= 1 ulp from CUDA's log (tests/test_gpu_fastlog.py checks the same
+// construction); table read through L1 from global memory (rare path only).
+__device__ __noinline__ double fast_log_g(double x) {
+  const uint64_t ix = (uint64_t)__double_as_longlong(x);
+  if (ix < 0x0010000000000000ull || ix >= 0x7ff0000000000000ull) return log(x);
+  const uint64_t tmp = ix - kLogOff;
+  const int i = (int)((tmp >> (52 - kLogTableBits)) & ((1u << kLogTableBits) - 1));
+  const int k = (int)((int64_t)tmp >> 52);
+  const double z = __longlong_as_double((long long)(ix - (tmp & 0xfff0000000000000ull)));
+  const double c = kLogTable[i][0], invc = kLogTable[i][1];
+  const double d = z - c;
+  const double rh = d * invc;
+  const double rl = fma(-rh, c, d) * invc;
+  double q = -0.125;
+  q = fma(q, rh, 1.0 / 7.0);
+  q = fma(q, rh, -1.0 / 6.0);
+  q = fma(q, rh, 0.2);
+  q = fma(q, rh, -0.25);
+  q = fma(q, rh, 1.0 / 3.0);
+  q = fma(q, rh, -0.5);
+  const double kd = (double)k;
+  double s1, e1, s2, e2;
+  two_sum_x(kd * kLn2Hi, kLogTable[i][2], s1, e1);
+  two_sum_x(s1, rh, s2, e2);
+  double lo = e1 + e2 + (kd * kLn2Lo + kLogTable[i][3]) + rl;
+  lo = fma(rh * rh, q, lo);
+  return s2 + lo;
+}
+
+// n and the direction of one pixel with the reference's f64 formulas
+// (model.py:125-137); returns n (0: no crossing) and |diff|, th.
+__device__ __noinline__ int exact_count(float v, float r, float thp, float thn, double log_eps, bool& pos,
+                                        double& ad, double& thd) {
+  const double ln = fast_log_g((double)v + log_eps);  // model.py:39
+  const double diff = ln - (double)r;
+  pos = diff > 0.0;
+  if (!(diff != 0.0) || diff != diff) return 0;
+  thd = (double)(pos ? thp : thn);
+  ad = pos ? diff : -diff;
+  const double q = __dadd_rn(__ddiv_rn(ad, thd), 1e-4);  // int(|diff|/th + 1e-4)
+  if (!(q >= 1.0)) return 0;
+  return q > 2147483647.0 ? 2147483647 : (int)q;
+}
+// t_rel of crossing j (model.py:144-146)
+__device__ __forceinline__ int exact_trel(int j, double thd, double ad, double dtd, int dtm1) {
+  const double a = __dmul_rn(__ddiv_rn(__dmul_rn((double)j, thd), ad), dtd);
+  const int tr = a >= (double)dtm1 ? dtm1 : (int)a;
+  return tr;
+}
+
+// ---------------------------------------------------------------------------
+// certified f32 lane math
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// |df - diff_ref| <= kEpsD + 3*2^-24*|df| (see the header comment of
+// fast_path.cuh); diff_ref is the reference's f64 ln(v + eps) - ref.
+// (kEpsD = 8e-9 enters the bands below as the 1e-8 terms.)
+
+struct LiteOut {
+  float uf;    // t_rel(j) ~ j * uf
+  float erel;  // relative band of j * uf
+};
+
+// All roundings below are explicit (_rn intrinsics / fmaf) so that no FMA
+// contraction can differ between the passes that evaluate the same pixel
+// (K1's count pass, its emission pass, and k_fast_redo): the decisions must
+// be bit-identical wherever they are recomputed.
+//
+// Returns n (>= 0) or -1 when the exact path must decide.
+__device__ __forceinline__ int lite_count(float v, float r, float thp, float thn, float rthp, float rthn,
+                                          double log_eps, float dtf, bool& pos, LiteOut& o) {
+  const double x = __dadd_rn((double)v, log_eps);  // the reference's x exactly
+  const uint64_t ix = (uint64_t)__double_as_longlong(x);
+  if (ix < 0x0010000000000000ull || ix >= 0x7ff0000000000000ull) return -1;
+  const uint64_t tmp = ix - kLogOff;
+  const int i = (int)((tmp >> (52 - kLogTableBits)) & ((1u << kLogTableBits) - 1));
+  const int k = (int)((int64_t)tmp >> 52);
+  const double z = __longlong_as_double((long long)(ix - (tmp & 0xfff0000000000000ull)));
+  const double d = __dsub_rn(z, kLogTable[i][0]);                       // exact
+  const float rf = __double2float_rn(__dmul_rn(d, kLogTable[i][1]));    // |r| <= 2^-7
+  float pf = fmaf(rf, 0.2f, -0.25f);
+  pf = fmaf(pf, rf, 0.33333334f);
+  pf = fmaf(pf, rf, -0.5f);
+  pf = fmaf(pf, rf, 1.0f);
+  pf = __fmul_rn(pf, rf);                                               // log1p(r), |err| < 2^-30
+  const double dd = __dsub_rn(fma((double)k, 0.6931471805599453, kLogTable[i][2]), (double)r);
+  const float df = __fadd_rn(__double2float_rn(dd), pf);
+  pos = df > 0.f;
+  const float ad = fabsf(df);
+  const float th = pos ? thp : thn;
+  const float rth = pos ? rthp : rthn;
+  const float q1 = fmaf(ad, rth, 1e-4f);  // |diff|/th + 1e-4 (model.py:137)
+  const float dn = fmaf(q1, 6e-7f, fmaf(1e-8f, rth, 1e-10f));
+  const float nlo = floorf(__fsub_rn(q1, dn)), nhi = floorf(__fadd_rn(q1, dn));
+  if (nlo != nhi || q1 > 1e6f) return -1;
+  const int n = (int)nlo;
+  if (n <= 0) return 0;
+  const float ra = rcp_approx(ad);
+  o.uf = __fmul_rn(__fmul_rn(th, dtf), ra);
+  o.erel = fmaf(1e-8f, ra, 1e-6f);
+  return n;
+}
+
+// certified floor of j*uf clamped to dt-1; -1 if the band straddles
+__device__ __forceinline__ int lite_trel(int j, const LiteOut& o, int dtm1) {
+  const float a = __fmul_rn((float)j, o.uf);
+  const float band = fmaf(a, o.erel, 1e-6f);
+  const int lo = min((int)floorf(__fsub_rn(a, band)), dtm1);
+  const int hi = min((int)floorf(__fadd_rn(a, band)), dtm1);
+  return lo == hi ? lo : -1;
+}
+
+// Per-frame constants of the lane math.
+struct FrameCtx {
+  double log_eps, dtd;
+  float log_eps_f, dtf;
+  int dtm1, tpr, refr;  // tpr: frame start relative to the call's time base
+};
+
+// One pixel, one frame (model.py:124-163): n (level steps), kept crossings
+// after the refractory filter, and the last kept time.
+struct PxStep {
+  int n, kept, lnew;
+  bool pos, exact;
+  LiteOut lo;
+};
+
+template <bool REFR>
+__device__ __forceinline__ void px_step(float v, float r, int lrel, float thp, float thn, float rthp, float rthn,
+                                        const FrameCtx& c, PxStep& o) {
+  o.n = 0;
+  o.kept = 0;
+  o.lnew = lrel;
+  {
+    // f32 prefilter: |__logf - ln| <= 2^-21 |ln| + 2^-22 and the f32 rounding of
+    // v + eps are far inside the margin, so a skipped pixel surely has n == 0
+    const float lf = __logf(v + c.log_eps_f);
+    const float d32 = lf - r;
+    const float th32 = d32 > 0.f ? thp : thn;
+    if (fabsf(d32) + (2e-6f * fabsf(lf) + 2e-6f) < th32 * (1.0f - 1e-4f)) return;
+  }
+  int n = lite_count(v, r, thp, thn, rthp, rthn, c.log_eps, c.dtf, o.pos, o.lo);
+  bool exact = n < 0;
+  int kept = 0, l = lrel;
+  if (!exact && n > 0) {
+    for (int j = 1; j <= n; ++j) {
+      const int tr = lite_trel(j, o.lo, c.dtm1);
+      if (tr < 0) { exact = true; break; }
+      if (REFR && c.tpr + tr - l < c.refr) continue;  // model.py:148-149
+      l = c.tpr + tr;
+      ++kept;
+    }
+  }
+  if (exact) {
+    double ad = 0.0, thd = 0.0;
+    n = exact_count(v, r, thp, thn, c.log_eps, o.pos, ad, thd);
+    kept = 0;
+    l = lrel;
+    for (int j = 1; j <= n; ++j) {
+      const int tr = exact_trel(j, thd, ad, c.dtd, c.dtm1);
+      if (REFR && c.tpr + tr - l < c.refr) continue;
+      l = c.tpr + tr;
+      ++kept;
+    }
+  }
+  o.n = n > 0 ? n : 0;
+  o.kept = kept;
+  o.lnew = l;
+  o.exact = exact;
+}
+
+// The kept crossing times of a pixel (chronological), as decided by px_step.
+template <bool REFR, typename Sink>
+__device__ __forceinline__ void px_emit(float v, float rold, int lold, float thp, float thn, int n, bool exact,
+                                        const LiteOut& lo, const FrameCtx& c, Sink&& sink) {
+  double ad = 0.0, thd = 0.0;
+  if (exact) {
+    bool p2;
+    exact_count(v, rold, thp, thn, c.log_eps, p2, ad, thd);
+  }
+  int l = lold;
+  for (int j = 1; j <= n; ++j) {
+    const int tr = exact ? exact_trel(j, thd, ad, c.dtd, c.dtm1) : lite_trel(j, lo, c.dtm1);
+    if (REFR) {
+      if (c.tpr + tr - l < c.refr) continue;
+      l = c.tpr + tr;
+    }
+    sink(tr);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int64_t frame_tprev(const FastArgs& a, int s, int f, int64_t t0c) {
+  return a.t_bounds ? a.t_bounds[(int64_t)s * (a.T + 1) + f] : t0c + (int64_t)f * a.tick;
+}
+__device__ __forceinline__ int64_t frame_tnow(const FastArgs& a, int s, int f, int64_t t0c) {
+  return a.t_bounds ? a.t_bounds[(int64_t)s * (a.T + 1) + f + 1] : t0c + (int64_t)(f + 1) * a.tick;
+}
+__device__ __forceinline__ FrameCtx frame_ctx(const FastArgs& a, int s, int f, int64_t t0c, int64_t tb) {
+  FrameCtx c;
+  const int64_t tprev = frame_tprev(a, s, f, t0c);
+  const int dt = (int)(frame_tnow(a, s, f, t0c) - tprev);
+  c.log_eps = a.log_eps;
+  c.log_eps_f = a.log_eps_f;
+  c.dtd = (double)dt;
+  c.dtf = (float)dt;
+  c.dtm1 = dt - 1;
+  c.tpr = (int)(tprev - tb);
+  c.refr = a.refr;
+  return c;
+}
+__device__ __forceinline__ int clamp_rel(int64_t d) {
+  return d < -(1ll << 30) ? -(1 << 30) : (d > (1ll << 30) ? (1 << 30) : (int)d);
+}
+
+template <bool REFR, bool UNI>
+__global__ void __launch_bounds__(kFNT, 2) k_fast_gen(FastArgs a) {
+  constexpr int NT = kFNT, VPT = kFVpt, NW = NT / 32, KB = kFMaxBuckets;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* s_list = reinterpret_cast<uint32_t*>(smem_raw);  // [kFListCap] pixel-major keys
+  uint32_t* s_sorted = s_list + kFListCap;                     // [kFListCap] bucket-sorted keys
+  uint32_t* s_wcnt = s_sorted + kFListCap;                     // [NW][KB] per-warp bucket counters
+  float* s_uf = reinterpret_cast<float*>(s_wcnt + NW * KB);    // [kFGmax] per-pixel carry to the emission:
+  float* s_erel = s_uf + kFGmax;                               //   lite step and band
+  int* s_meta = reinterpret_cast<int*>(s_erel + kFGmax);       //   n | exact << 24
+  int* s_lold = s_meta + kFGmax;                               //   last event before the frame
+  float* s_rold = reinterpret_cast<float*>(s_lold + kFGmax);   //   level before the frame
+  __shared__ uint32_t s_bstart[KB + 1];
+  __shared__ int s_scan[NW + 1];
+  __shared__ uint32_t s_res2[2];  // per frame parity (read + reset without a trailing barrier)
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int s = blockIdx.x / a.ntiles;
+  const int tile = blockIdx.x % a.ntiles;
+  const int64_t P = a.P;
+  const int64_t tile0 = (int64_t)tile * a.G;
+  const int gt = (int)min((int64_t)a.G, P - tile0);  // pixels of this tile
+  const int lp0 = tid * VPT;                        // first local pixel of this thread
+  const int64_t pix0 = tile0 + lp0;
+  const bool full = (lp0 + VPT <= gt) && a.vec;
+  float* refp = a.ref + (int64_t)s * P;
+  int64_t* lastp = a.last + (int64_t)s * P;
+  const int64_t t0c = a.desc ? a.desc->cur_t0 : a.t0;
+  const int64_t tb = frame_tprev(a, s, 0, t0c);  // time base of the relative times
+  const int nbk = a.nbk;
+
+  // ---- state into registers ----
+  float r[VPT], thp[VPT], thn[VPT], rthp[VPT], rthn[VPT];
+  int lrel[VPT];
+  uint32_t dirty = 0;  // bit k: level changed, bit 4+k: last event changed
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    r[k] = 0.f; lrel[k] = -(1 << 30);
+    thp[k] = a.thp_u; thn[k] = a.thn_u; rthp[k] = a.rthp_u; rthn[k] = a.rthn_u;
+  }
+  {
+    int64_t lt[VPT];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) lt[k] = 0;
+    if (full) {
+      const float4 q = __ldcg(reinterpret_cast<const float4*>(refp + pix0));
+      r[0] = q.x; r[1] = q.y; r[2] = q.z; r[3] = q.w;
+      if (REFR) {
+        const longlong2 l0 = __ldcg(reinterpret_cast<const longlong2*>(lastp + pix0));
+        const longlong2 l1 = __ldcg(reinterpret_cast<const longlong2*>(lastp + pix0 + 2));
+        lt[0] = l0.x; lt[1] = l0.y; lt[2] = l1.x; lt[3] = l1.y;
+      }
+      if (!UNI) {
+        const float4 p4 = *reinterpret_cast<const float4*>(a.thp + (int64_t)s * P + pix0);
+        const float4 n4 = *reinterpret_cast<const float4*>(a.thn + (int64_t)s * P + pix0);
+        thp[0] = p4.x; thp[1] = p4.y; thp[2] = p4.z; thp[3] = p4.w;
+        thn[0] = n4.x; thn[1] = n4.y; thn[2] = n4.z; thn[3] = n4.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        if (lp0 + k < gt) {
+          r[k] = __ldcg(refp + pix0 + k);
+          if (REFR) lt[k] = __ldcg(lastp + pix0 + k);
+          if (!UNI) { thp[k] = a.thp[(int64_t)s * P + pix0 + k]; thn[k] = a.thn[(int64_t)s * P + pix0 + k]; }
+        }
+      }
+    }
+    if (REFR) {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) lrel[k] = clamp_rel(lt[k] - tb);
+    }
+    if (!UNI) {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) { rthp[k] = __frcp_rn(thp[k]); rthn[k] = __frcp_rn(thn[k]); }
+    }
+  }
+  for (int i = tid; i < NW * KB; i += NT) s_wcnt[i] = 0;
+  if (tid < 2) s_res2[tid] = 0;
+
+  auto load_frame = [&](int f, float* dst) {
+    const float* fr = a.frames + ((int64_t)s * a.T + f) * P;
+    if (full) {
+      const float4 q = __ldcs(reinterpret_cast<const float4*>(fr + pix0));
+      dst[0] = q.x; dst[1] = q.y; dst[2] = q.z; dst[3] = q.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) dst[k] = (lp0 + k < gt) ? __ldcs(fr + pix0 + k) : 1.0f;
+    }
+  };
+  float vnext[VPT];
+  load_frame(0, vnext);
+  __syncthreads();
+
+  for (int f = 0; f < a.T; ++f) {
+    const int seg = s * a.T + f;
+    const FrameCtx c = frame_ctx(a, s, f, t0c, tb);
+    uint32_t& s_res = s_res2[f & 1];
+    float v[VPT];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) v[k] = vnext[k];
+    if (f + 1 < a.T) load_frame(f + 1, vnext);
+
+    // ---- 1. lane math: crossings, refractory, new state ----
+    uint32_t emask = 0;  // bit k: pixel k has kept crossings; bit 4+k: its level changed
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      if (lp0 + k >= gt) continue;
+      PxStep o;
+      px_step<REFR>(v[k], r[k], lrel[k], thp[k], thn[k], rthp[k], rthn[k], c, o);
+      if (o.n == 0) continue;
+      const int lp = lp0 + k;
+      s_rold[lp] = r[k];
+      s_lold[lp] = lrel[k];
+      // new level f32(ls +- n*th) (model.py:159-162); n*th is exact in f64
+      const double step = __dmul_rn((double)o.n, (double)(o.pos ? thp[k] : thn[k]));
+      r[k] = __double2float_rn(o.pos ? __dadd_rn((double)r[k], step) : __dsub_rn((double)r[k], step));
+      dirty |= 1u << k;
+      emask |= 16u << k;
+      if (o.kept > 0) {
+        lrel[k] = o.lnew;
+        dirty |= 16u << k;
+        emask |= 1u << k;
+        s_uf[lp] = o.lo.uf;
+        s_erel[lp] = o.lo.erel;
+        s_meta[lp] = min(o.n, 0x7fffff) | (o.pos ? (1 << 23) : 0) | (o.exact ? (1 << 24) : 0);
+      }
+      cnt += o.kept;
+    }
+    // 32-pixel chunks with >= 1 kept event (AggregationStats.reservation_count):
+    // a chunk is 8 consecutive lanes; tiles start on chunk boundaries
+    {
+      const uint32_t b = __ballot_sync(0xffffffffu, cnt > 0);
+      if (lane == 0 && b) {
+        const uint32_t cc = ((b & 0xffu) != 0) + ((b & 0xff00u) != 0) + ((b & 0xff0000u) != 0) +
+                            ((b & 0xff000000u) != 0);
+        atomicAdd(&s_res, cc);
+      }
+    }
+    // ---- 2. pixel-major compaction ----
+    int total;
+    int off = block_excl_scan<NT, int>(cnt, s_scan, &total);
+    const int wbeg = __shfl_sync(0xffffffffu, off, 0);
+    const int wend = __shfl_sync(0xffffffffu, off + cnt, 31);
+    const int64_t st_idx = (int64_t)seg * a.ntiles + tile;
+    if (total > kFListCap) {  // block-uniform, rare: k_fast_redo regenerates this tile-frame
+      float* sr = a.snap_ref + st_idx * a.G;
+      int* sl = a.snap_last + st_idx * a.G;
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        const int lp = lp0 + k;
+        if (lp >= gt) continue;
+        const bool ch = (emask >> (4 + k)) & 1u;
+        sr[lp] = ch ? s_rold[lp] : r[k];
+        sl[lp] = ch ? s_lold[lp] : lrel[k];
+      }
+      __syncthreads();
+      if (tid == 0) {
+        a.tile_src[st_idx] = kSrcRedo;
+        a.rows[((int64_t)seg * (nbk + 1) + nbk) * a.ntiles + tile] = (uint32_t)total;
+        if (s_res) atomicAdd(reinterpret_cast<unsigned long long*>(a.seg_res + seg), (unsigned long long)s_res);
+        s_res = 0;
+      }
+      __syncthreads();
+      continue;
+    }
+    if (emask & 0xfu) {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        if (!((emask >> k) & 1u)) continue;
+        const int lp = lp0 + k;
+        const int meta = s_meta[lp];
+        const uint32_t xyp = ((uint32_t)lp << 1) | ((meta >> 23) & 1u);
+        const LiteOut lo{s_uf[lp], s_erel[lp]};
+        px_emit<REFR>(v[k], s_rold[lp], s_lold[lp], thp[k], thn[k], meta & 0x7fffff, (meta >> 24) & 1, lo, c,
+                      [&](int tr) {
+                        s_list[off++] = ((uint32_t)tr << 12) | xyp;
+                        atomicAdd(&s_wcnt[warp * KB + (tr >> 3)], 1u);
+                      });
+      }
+    }
+    __syncthreads();
+
+    // ---- 3. bucket starts: column prefix over warps, exclusive scan over buckets ----
+    {
+      uint32_t tot = 0;
+      if (tid < nbk) {
+#pragma unroll 4
+        for (int w = 0; w < NW; ++w) {
+          const uint32_t cc = s_wcnt[w * KB + tid];
+          s_wcnt[w * KB + tid] = tot;
+          tot += cc;
+        }
+      }
+      int tt;
+      const uint32_t bst = (uint32_t)block_excl_scan<NT, int>((int)tot, s_scan, &tt);
+      if (tid < nbk) {
+#pragma unroll 4
+        for (int w = 0; w < NW; ++w) s_wcnt[w * KB + tid] += bst;
+        s_bstart[tid] = bst;
+      }
+      if (tid == 0) s_bstart[nbk] = (uint32_t)total;
+    }
+    __syncthreads();
+
+    // ---- 4. stable rank (warp match-any, pixel order) and scatter ----
+    for (int base = wbeg; base < wend; base += 32) {
+      const int i = base + lane;
+      const bool valid = i < wend;
+      const uint32_t active = __ballot_sync(0xffffffffu, valid);
+      if (valid) {
+        const uint32_t key = s_list[i];
+        const int bk = (int)(key >> 15);
+        const uint32_t peers = __match_any_sync(active, bk);
+        const int leader = __ffs(peers) - 1;
+        uint32_t bpos = 0;
+        if (lane == leader) {
+          bpos = s_wcnt[warp * KB + bk];
+          s_wcnt[warp * KB + bk] = bpos + __popc(peers);
+        }
+        bpos = __shfl_sync(active, bpos, leader);
+        s_sorted[bpos + __popc(peers & lanemask_lt())] = key;
+      }
+    }
+    __syncthreads();
+
+    // ---- 5. sorted keys and bucket starts out; reset the counters ----
+    {
+      uint32_t* dst = a.keys + st_idx * kFListCap;
+      const int n4 = total >> 2;
+      for (int i = tid; i < n4; i += NT)
+        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(s_sorted)[i];
+      for (int i = 4 * n4 + tid; i < total; i += NT) dst[i] = s_sorted[i];
+      uint32_t* rows = a.rows + (int64_t)seg * (nbk + 1) * a.ntiles + tile;
+      for (int b = tid; b <= nbk; b += NT) rows[(int64_t)b * a.ntiles] = s_bstart[b];
+      for (int i = tid; i < NW * KB; i += NT) s_wcnt[i] = 0;
+      if (tid == 0) {
+        a.tile_src[st_idx] = kSrcSlot;
+        if (s_res) atomicAdd(reinterpret_cast<unsigned long long*>(a.seg_res + seg), (unsigned long long)s_res);
+        s_res = 0;
+      }
+    }
+  }
+
+  // ---- state write-back (the prologue validated every frame of the call) ----
+  if (*a.bad == kNoBad) {
+    if (full && (dirty & 0xfu) == 0xfu) {
+      *reinterpret_cast<float4*>(refp + pix0) = make_float4(r[0], r[1], r[2], r[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k)
+        if (dirty & (1u << k)) refp[pix0 + k] = r[k];
+    }
+    if (full && (dirty & 0xf0u) == 0xf0u) {
+      *reinterpret_cast<longlong2*>(lastp + pix0) = make_longlong2(tb + lrel[0], tb + lrel[1]);
+      *reinterpret_cast<longlong2*>(lastp + pix0 + 2) = make_longlong2(tb + lrel[2], tb + lrel[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k)
+        if (dirty & (16u << k)) lastp[pix0 + k] = tb + lrel[k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fixup (one CTA per segment): totals, counts / dropped, capacity cut, and the
+// work list of tile-frames K1 could not hold (regenerated by k_fast_redo)
+// ---------------------------------------------------------------------------
+constexpr int kFixNT = 512;
+
+__device__ __forceinline__ const uint32_t* tile_keys(const FastArgs& a, int seg, int q) {
+  const int64_t st = (int64_t)seg * a.ntiles + q;
+  const int64_t src = a.tile_src[st];
+  return src < 0 ? a.keys + st * kFListCap : a.area_sorted + (int64_t)seg * a.cap + src;
+}
+
+__global__ void __launch_bounds__(kFixNT) k_fast_fix(FastArgs a) {
+  constexpr int NT = kFixNT;
+  __shared__ int64_t s_scan64[NT / 32 + 1];
+  __shared__ int s_scan[NT / 32 + 1];
+  __shared__ uint32_t s_hist[kFMaxBuckets + 1];
+  __shared__ int s_qcut;
+  __shared__ int64_t s_qbase;
+  const int seg = blockIdx.x, tid = threadIdx.x;
+  const int nbk = a.nbk, nt = a.ntiles;
+  uint32_t* rows = a.rows + (int64_t)seg * (nbk + 1) * nt;
+  const int64_t* src = a.tile_src + (int64_t)seg * nt;
+  if (*a.bad != kNoBad) {
+    if (tid == 0) { a.out_count[seg] = 0; a.out_dropped[seg] = 0; a.redo_n[seg] = 0; }
+    return;
+  }
+  const int64_t cap = a.cap;
+  if (tid == 0) s_qcut = nt;
+  // pixel-major base of every tile; the tile holding the cut; the redo list
+  int64_t run = 0;
+  int redo_run = 0;
+  int64_t area_run = 0;
+  for (int q0 = 0; q0 < nt; q0 += NT) {
+    const int q = q0 + tid;
+    const int64_t c = q < nt ? (int64_t)rows[(int64_t)nbk * nt + q] : 0;
+    int64_t tt;
+    const int64_t base = run + block_excl_scan<NT, int64_t>(c, s_scan64, &tt);
+    run += tt;
+    const bool redo = q < nt && src[q] == kSrcRedo && base < cap;
+    const int64_t lim = redo ? (base + c > cap ? cap - base : c) : 0;
+    if (q < nt && base < cap && base + c > cap) s_qcut = q;  // unique
+    int ntt;
+    const int rex = block_excl_scan<NT, int>(redo ? 1 : 0, s_scan, &ntt);
+    int64_t att;
+    const int64_t aex = block_excl_scan<NT, int64_t>(lim, s_scan64, &att);
+    if (redo) {
+      int* item = a.redo_items + ((int64_t)seg * nt + redo_run + rex) * 2;
+      item[0] = q;
+      item[1] = (int)(area_run + aex);
+      a.redo_lim[(int64_t)seg * nt + q] = (int)lim;
+    }
+    redo_run += ntt;
+    area_run += att;
+  }
+  const int64_t total = run;
+  __syncthreads();
+  const int qc = s_qcut;
+  if (total > cap) {
+    // capacity (model.py:150-158): tiles after the cut keep nothing
+    for (int q = qc + 1; q < nt; ++q)
+      for (int b = tid; b <= nbk; b += NT) rows[(int64_t)b * nt + q] = 0;
+    if (src[qc] != kSrcRedo) {
+      // cut inside a K1 tile list: keep its first `keepn` events in pixel-major
+      // order = order by (pixel, t_rel); identical keys are interchangeable
+      if (tid == 0) {
+        int64_t r2 = 0;
+        for (int q = 0; q < qc; ++q) r2 += rows[(int64_t)nbk * nt + q];
+        s_qbase = r2;
+      }
+      __syncthreads();
+      const int64_t keepn = cap - s_qbase;
+      const int n = (int)rows[(int64_t)nbk * nt + qc];
+      uint32_t* list = a.keys + ((int64_t)seg * nt + qc) * kFListCap;
+      for (int i = tid; i < n; i += NT) {
+        const uint32_t ki = list[i];
+        const uint32_t pi = ((ki >> 1) & 0x7ffu) << 12 | (ki >> 12);
+        int rank = 0;
+        for (int j = 0; j < n; ++j) {
+          const uint32_t kj = list[j] & 0x7fffffffu;
+          const uint32_t pj = ((kj >> 1) & 0x7ffu) << 12 | (kj >> 12);
+          rank += (pj < pi) || (pj == pi && j < i);
+        }
+        if (rank < keepn) list[i] = ki | 0x80000000u;
+      }
+      __syncthreads();
+      // stable in-place compaction of the kept keys, then the tile's bucket starts
+      for (int b = tid; b <= nbk; b += NT) s_hist[b] = 0;
+      int kr = 0;
+      for (int base = 0; base < n; base += NT) {
+        const int i = base + tid;
+        const uint32_t k = i < n ? list[i] : 0u;
+        const int keep = (k >> 31) & 1;
+        int tt;
+        const int ex = block_excl_scan<NT, int>(keep, s_scan, &tt);
+        if (keep) {
+          list[kr + ex] = k & 0x7fffffffu;
+          atomicAdd(&s_hist[(k & 0x7fffffffu) >> 15], 1u);
+        }
+        kr += tt;
+        __syncthreads();
+      }
+      const int cc = tid < nbk ? (int)s_hist[tid] : 0;
+      int tt;
+      const int ex = block_excl_scan<NT, int>(cc, s_scan, &tt);
+      if (tid < nbk) rows[(int64_t)tid * nt + qc] = (uint32_t)ex;
+      if (tid == 0) rows[(int64_t)nbk * nt + qc] = (uint32_t)tt;
+    }
+  }
+  if (tid == 0) {
+    const int64_t written = total < cap ? total : cap;
+    a.out_count[seg] = written;
+    a.out_dropped[seg] = total - written;
+    a.redo_n[seg] = redo_run;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// redo: regenerate a tile-frame whose crossings overflowed K1's shared list,
+// from the state snapshot K1 left, keeping at most its capacity share; stable
+// bucket sort into the segment's overflow area.  Grid (kRedoCtas, nseg).
+// ---------------------------------------------------------------------------
+constexpr int kRedoNT = 256, kRedoCtas = 8;
+
+template <bool REFR>
+__global__ void __launch_bounds__(kRedoNT) k_fast_redo(FastArgs a) {
+  constexpr int NT = kRedoNT, PPT = (kFGmax + NT - 1) / NT;
+  __shared__ int s_scan[NT / 32 + 1];
+  __shared__ uint32_t s_hist[kFMaxBuckets + 1];
+  const int seg = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
+  if (*a.bad != kNoBad) return;
+  const int nitems = a.redo_n[seg];
+  const int s = seg / a.T, f = seg % a.T;
+  const int nbk = a.nbk, nt = a.ntiles;
+  const int64_t t0c = a.desc ? a.desc->cur_t0 : a.t0;
+  const int64_t tb = frame_tprev(a, s, 0, t0c);
+  const FrameCtx c = frame_ctx(a, s, f, t0c, tb);
+  uint32_t* rows = a.rows + (int64_t)seg * (nbk + 1) * nt;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int q = a.redo_items[((int64_t)seg * nt + it) * 2];
+    const int aoff = a.redo_items[((int64_t)seg * nt + it) * 2 + 1];
+    const int lim = a.redo_lim[(int64_t)seg * nt + q];
+    const int64_t st_idx = (int64_t)seg * nt + q;
+    const int64_t tile0 = (int64_t)q * a.G;
+    const int gt = (int)min((int64_t)a.G, a.P - tile0);
+    const float* sr = a.snap_ref + st_idx * a.G;
+    const int* sl = a.snap_last + st_idx * a.G;
+    const float* fr = a.frames + ((int64_t)s * a.T + f) * a.P + tile0;
+    const float* tp = a.thp ? a.thp + (int64_t)s * a.P + tile0 : nullptr;
+    const float* tn = a.thn ? a.thn + (int64_t)s * a.P + tile0 : nullptr;
+    uint32_t* un = a.area_unsorted + (int64_t)seg * a.cap + aoff;
+    uint32_t* so = a.area_sorted + (int64_t)seg * a.cap + aoff;
+    // pass 1: pixel-major emission (thread owns PPT consecutive pixels)
+    int cnt = 0;
+    const int lp0 = tid * PPT;
+    for (int k = 0; k < PPT; ++k) {
+      const int lp = lp0 + k;
+      if (lp >= gt) break;
+      const float thp = tp ? tp[lp] : a.thp_u, thn = tn ? tn[lp] : a.thn_u;
+      const float rthp = tp ? __frcp_rn(thp) : a.rthp_u, rthn = tn ? __frcp_rn(thn) : a.rthn_u;
+      PxStep o;
+      px_step<REFR>(fr[lp], sr[lp], sl[lp], thp, thn, rthp, rthn, c, o);
+      cnt += o.kept;
+    }
+    int total;
+    int off = block_excl_scan<NT, int>(cnt, s_scan, &total);
+    for (int k = 0; k < PPT && off < lim; ++k) {
+      const int lp = lp0 + k;
+      if (lp >= gt) break;
+      const float thp = tp ? tp[lp] : a.thp_u, thn = tn ? tn[lp] : a.thn_u;
+      const float rthp = tp ? __frcp_rn(thp) : a.rthp_u, rthn = tn ? __frcp_rn(thn) : a.rthn_u;
+      PxStep o;
+      px_step<REFR>(fr[lp], sr[lp], sl[lp], thp, thn, rthp, rthn, c, o);
+      if (o.kept == 0) continue;
+      const uint32_t xyp = ((uint32_t)lp << 1) | (o.pos ? 1u : 0u);
+      px_emit<REFR>(fr[lp], sr[lp], sl[lp], thp, thn, o.n, o.exact, o.lo, c, [&](int tr) {
+        if (off < lim) un[off] = ((uint32_t)tr << 12) | xyp;
+        ++off;
+      });
+    }
+    for (int b = tid; b <= nbk; b += NT) s_hist[b] = 0;
+    __syncthreads();
+    for (int i = tid; i < lim; i += NT) atomicAdd(&s_hist[un[i] >> 15], 1u);
+    __syncthreads();
+    {
+      const int cc = tid < nbk ? (int)s_hist[tid] : 0;
+      int tt;
+      const int ex = block_excl_scan<NT, int>(cc, s_scan, &tt);
+      if (tid < nbk) { s_hist[tid] = (uint32_t)ex; rows[(int64_t)tid * nt + q] = (uint32_t)ex; }
+      if (tid == 0) rows[(int64_t)nbk * nt + q] = (uint32_t)lim;
+    }
+    __syncthreads();
+    if (tid < 32) {  // one warp in list order: stable
+      for (int base = 0; base < lim; base += 32) {
+        const int i = base + lane;
+        const bool valid = i < lim;
+        const uint32_t active = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+          const uint32_t key = un[i];
+          const int bk = (int)(key >> 15);
+          const uint32_t peers = __match_any_sync(active, bk);
+          const int leader = __ffs(peers) - 1;
+          uint32_t bpos = 0;
+          if (lane == leader) { bpos = s_hist[bk]; s_hist[bk] = bpos + __popc(peers); }
+          bpos = __shfl_sync(active, bpos, leader);
+          so[bpos + __popc(peers & lanemask_lt())] = key;
+        }
+        __syncwarp();
+      }
+    }
+    if (tid == 0) a.tile_src[st_idx] = aoff;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: one CTA per (segment, bucket of 8 t_rel bins)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void bucket_place(const uint32_t* in, uint32_t* out, int n, int* binstart,
+                                             uint32_t* bintot, uint64_t* s_scan64) {
+  // stable counting sort of in[0..n) by bits 25-27 (t_rel within the bucket)
+  constexpr int NT = kONT;
+  const int tid = threadIdx.x;
+  const int m = (n + NT - 1) / NT;
+  const int i0 = min(n, tid * m), i1 = min(n, i0 + m);
+  uint64_t lo = 0, hi = 0;  // 8 x 16-bit counters
+  for (int i = i0; i < i1; ++i) {
+    const uint32_t b = (in[i] >> 25) & 7u;
+    if (b < 4) lo += 1ull << (16 * b); else hi += 1ull << (16 * (b - 4));
+  }
+  uint64_t tlo, thi;
+  const uint64_t plo = block_excl_scan<NT, uint64_t>(lo, s_scan64, &tlo);
+  const uint64_t phi = block_excl_scan<NT, uint64_t>(hi, s_scan64, &thi);
+  uint32_t st[8];
+  uint32_t acc = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const uint32_t t = (uint32_t)(((b < 4 ? tlo : thi) >> (16 * (b & 3))) & 0xffffu);
+    st[b] = acc + (uint32_t)(((b < 4 ? plo : phi) >> (16 * (b & 3))) & 0xffffu);
+    if (tid == 0) { binstart[b] = (int)acc; bintot[b] = t; }
+    acc += t;
+  }
+  for (int i = i0; i < i1; ++i) {
+    const uint32_t e = in[i];
+    const uint32_t b = (e >> 25) & 7u;
+    uint32_t pos = st[0];
+#pragma unroll
+    for (int cc = 1; cc < 8; ++cc) pos = b == (uint32_t)cc ? st[cc] : pos;
+    out[pos] = e;
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) st[cc] += b == (uint32_t)cc ? 1u : 0u;
+  }
+}
+
+__global__ void __launch_bounds__(kONT, 2) k_fast_order(FastArgs a) {
+  constexpr int NT = kONT, NW = NT / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* s_g = reinterpret_cast<uint32_t*>(smem_raw);  // [kOCap] gathered entries
+  uint32_t* s_s = s_g + kOCap;                             // [kOCap] bin-sorted entries
+  int* s_goff = reinterpret_cast<int*>(s_s + kOCap);       // [ntiles + 1]
+  int* s_s0 = s_goff + a.ntiles + 1;                       // [ntiles]
+  __shared__ uint64_t s_scan64[NW + 1];
+  __shared__ int64_t s_red[NW + 1];
+  __shared__ int s_scan[NW + 1];
+  __shared__ int s_binstart[8];
+  __shared__ uint32_t s_bintot[8];
+  __shared__ int64_t s_gbs[8];
+  __shared__ int64_t s_grun[8];
+  __shared__ uint32_t s_cnt[8];
+
+  const int seg = blockIdx.y, k = blockIdx.x, tid = threadIdx.x;
+  if (*a.bad != kNoBad) return;
+  const int nbk = a.nbk, nt = a.ntiles;
+  const int s = seg / a.T, f = seg % a.T;
+  const uint32_t* rows = a.rows + (int64_t)seg * (nbk + 1) * nt;
+  const int64_t t0c = a.desc ? a.desc->cur_t0 : a.t0;
+  const int64_t tbin0 = frame_tprev(a, s, f, t0c) + 8 * k;
+
+  // slice of every tile, gather offsets, and the bucket's base in the segment
+  int64_t base_part = 0;
+  int run = 0;
+  for (int q0 = 0; q0 < nt; q0 += NT) {
+    const int q = q0 + tid;
+    int len = 0;
+    if (q < nt) {
+      const uint32_t s0 = rows[(int64_t)k * nt + q];
+      const uint32_t s1 = rows[(int64_t)(k + 1) * nt + q];
+      s_s0[q] = (int)s0;
+      len = (int)(s1 - s0);
+      base_part += s0;
+    }
+    int tt;
+    const int ex = block_excl_scan<NT, int>(len, s_scan, &tt);
+    if (q < nt) s_goff[q] = run + ex;
+    run += tt;
+  }
+  const int total = run;
+  if (tid == 0) s_goff[nt] = total;
+  int64_t base;
+  block_excl_scan<NT, int64_t>(base_part, s_red, &base);  // (syncs)
+  if (total == 0) return;
+  const int64_t ob = (int64_t)seg * a.seg_stride + base;
+  const bool multi = total > kOCap;
+  if (multi) {
+    // pass A: bin totals of the whole bucket
+    if (tid < 8) s_cnt[tid] = 0;
+    __syncthreads();
+    for (int q = tid >> 3; q < nt; q += NT / 8) {
+      const int len = s_goff[q + 1] - s_goff[q];
+      const uint32_t* srcp = tile_keys(a, seg, q) + s_s0[q];
+      for (int j = tid & 7; j < len; j += 8) atomicAdd(&s_cnt[(srcp[j] >> 12) & 7u], 1u);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int64_t acc = 0;
+      for (int b = 0; b < 8; ++b) { s_gbs[b] = acc; s_grun[b] = 0; acc += s_cnt[b]; }
+    }
+    __syncthreads();
+  }
+  const int W = a.W;
+  const float winv = 1.0f / (float)W;
+  for (int g0 = 0; g0 < total; g0 += kOCap) {
+    const int n = min(kOCap, total - g0);
+    // gather: 8 lanes per tile, tiles overlapping [g0, g0 + n)
+    int qa = 0;
+    {
+      int lo = 0, hi = nt - 1;  // last q with goff[q] <= g0
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_goff[mid] <= g0) lo = mid; else hi = mid - 1;
+      }
+      qa = lo;
+    }
+    for (int q = qa + (tid >> 3); q < nt && s_goff[q] < g0 + n; q += NT / 8) {
+      const int gq0 = max(s_goff[q], g0), gq1 = min(s_goff[q + 1], g0 + n);
+      if (gq1 <= gq0) continue;
+      const uint32_t* srcp = tile_keys(a, seg, q) + s_s0[q] + (gq0 - s_goff[q]);
+      const uint32_t gpx0 = (uint32_t)q * (uint32_t)a.G;
+      for (int j = tid & 7; j < gq1 - gq0; j += 8) {
+        const uint32_t key = __ldcs(srcp + j);
+        // entry: pixel | p << 24 | (t_rel & 7) << 25
+        s_g[gq0 - g0 + j] = (gpx0 + ((key >> 1) & 0x7ffu)) | ((key & 1u) << 24) | (((key >> 12) & 7u) << 25);
+      }
+    }
+    __syncthreads();
+    bucket_place(s_g, s_s, n, s_binstart, s_bintot, s_scan64);
+    __syncthreads();
+    for (int i = tid; i < n; i += NT) {
+      const uint32_t e = s_s[i];
+      const uint32_t b = (e >> 25) & 7u;
+      const int64_t o = multi ? ob + s_gbs[b] + s_grun[b] + (i - s_binstart[b]) : ob + i;
+      const uint32_t gp = e & 0xffffffu;
+      uint32_t y = (uint32_t)((float)gp * winv);
+      if (y * (uint32_t)W > gp) --y;
+      else if ((y + 1) * (uint32_t)W <= gp) ++y;
+      a.out_t[o] = tbin0 + (int64_t)b;
+      a.out_x[o] = (uint16_t)(gp - y * (uint32_t)W);
+      a.out_y[o] = (uint16_t)y;
+      a.out_p[o] = (e >> 24) & 1u ? (int8_t)1 : (int8_t)-1;
+    }
+    __syncthreads();
+    if (multi && tid < 8) s_grun[tid] += s_bintot[tid];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+template <typename K>
+static void ensure_smem_fast(K k, size_t bytes) {
+  static const void* done[16];
+  static int ndone = 0;
+  const void* key = reinterpret_cast<const void*>(k);
+  for (int i = 0; i < ndone; ++i)
+    if (done[i] == key) return;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (ndone < 16) done[ndone++] = key;
+}
+
+size_t fast_gen_smem() { return (size_t)(2 * kFListCap + (kFNT / 32) * kFMaxBuckets + 5 * kFGmax) * 4; }
+size_t fast_order_smem(int ntiles) { return (size_t)2 * kOCap * 4 + (size_t)(2 * ntiles + 1) * 4; }
+
+cudaError_t launch_fast_gen(const FastArgs& a, cudaStream_t st) {
+  const size_t smem = fast_gen_smem();
+  const unsigned grid = (unsigned)((int64_t)a.S * a.ntiles);
+  const bool uni = a.thp == nullptr;
+  const bool refr = a.refr > 0;
+#define EVS_FAST_GEN(R, U)                        \
+  {                                               \
+    auto kf = k_fast_gen<R, U>;                   \
+    ensure_smem_fast(kf, fast_gen_smem()); \
+    kf<<<grid, kFNT, smem, st>>>(a);              \
+  }
+  if (refr) {
+    if (uni) EVS_FAST_GEN(true, true) else EVS_FAST_GEN(true, false)
+  } else {
+    if (uni) EVS_FAST_GEN(false, true) else EVS_FAST_GEN(false, false)
+  }
+#undef EVS_FAST_GEN
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fast_fix(const FastArgs& a, int nseg, cudaStream_t st) {
+  k_fast_fix<<<nseg, kFixNT, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fast_redo(const FastArgs& a, int nseg, cudaStream_t st) {
+  dim3 grid(kRedoCtas, nseg);
+  if (a.refr > 0) k_fast_redo<true><<<grid, kRedoNT, 0, st>>>(a);
+  else k_fast_redo<false><<<grid, kRedoNT, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fast_order(const FastArgs& a, int nseg, cudaStream_t st) {
+  const size_t smem = fast_order_smem(a.ntiles);
+  ensure_smem_fast(k_fast_order, fast_order_smem(kFMaxTiles));
+  dim3 grid(a.nbk, nseg);
+  k_fast_order<<<grid, kONT, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace evs
