@@ -42,8 +42,9 @@ struct StepLayout {
       seg_tbase, seg_tile_prefix, status2, keysA, keysB, total;
   // fast canonical path (fast_path.cu)
   bool fast;
-  int fG, fntiles, fnbk;
-  size_t fkeys, frows, fsrc, fsnapr, fsnapl, fareau, fareas, fitems, flim, fredon;
+  int fG, fntiles, fnbk, fmaxp;
+  int64_t n2;
+  size_t fkeys, frows, fsrc, fsnapr, fsnapl, fareau, fareas, fitems, flim, fredon, fpieces, fnpieces, fpcnt;
 };
 
 // Fast path: canonical order, t_now - t_prev <= 2048 us, P < 2^24.  Tiles of
@@ -110,7 +111,11 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   size_t off = 0;
   L->ctr = off; off = align_up(off + 64 * sizeof(uint32_t));
   L->desc = off; off = align_up(off + sizeof(StepDesc));
-  L->zero2 = off; off = align_up(off + (ns + 1) * 8);  // ovf_cursor[nseg] + err
+  const bool fast_early = fast_shape(p, P, canon ? (p->max_dt > 0 ? p->max_dt : p->tick) : 0, &L->fG,
+                                     &L->fntiles, &L->fnbk);
+  // zeroed by the prologue: ovf_cursor[nseg] + err (+ fast path: bucket totals [nseg][nbk] u32)
+  L->n2 = (int64_t)ns + 1 + (fast_early ? ((int64_t)ns * L->fnbk + 1) / 2 : 0);
+  L->zero2 = off; off = align_up(off + (size_t)L->n2 * 8);
   L->chunk_flag = off; off = align_up(off + (size_t)p->streams * nt * 8);
   L->tile_count = off; off = align_up(off + ns * nt * 8);
   L->tile_ovf = off; off = align_up(off + ns * nt * 8);
@@ -142,6 +147,10 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
     L->fitems = off; off = align_up(off + ns * fnt * 8);
     L->flim = off; off = align_up(off + ns * fnt * 4);
     L->fredon = off; off = align_up(off + ns * 4);
+    L->fmaxp = L->fnbk + 2 * (int)((cap + kOCap - 1) / kOCap) + 2;
+    L->fpieces = off; off = align_up(off + ns * (size_t)L->fmaxp * 8 * 4);
+    L->fnpieces = off; off = align_up(off + ns * 4);
+    L->fpcnt = off; off = align_up(off + ns * (size_t)L->fmaxp * 8 * 4);
   }
   L->total = off;
   return true;
@@ -200,7 +209,7 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   mark(0);
   cudaError_t e = launch_prologue(b->frames, (int64_t)L.nseg * P, P, p->validate, b->bad_pixel,
                                   b->reservations, L.nseg, desc, (int64_t)p->frames * p->tick, zero2,
-                                  L.nseg + 1, st);
+                                  L.n2, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(1);
 
@@ -225,6 +234,9 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
     fa.snap_ref = at<float>(ws, L.fsnapr); fa.snap_last = at<int>(ws, L.fsnapl);
     fa.area_unsorted = at<uint32_t>(ws, L.fareau); fa.area_sorted = at<uint32_t>(ws, L.fareas);
     fa.redo_items = at<int>(ws, L.fitems); fa.redo_lim = at<int>(ws, L.flim); fa.redo_n = at<int>(ws, L.fredon);
+    fa.btot = reinterpret_cast<uint32_t*>(zero2 + L.nseg + 1);
+    fa.pieces = at<int>(ws, L.fpieces); fa.npieces = at<int>(ws, L.fnpieces);
+    fa.pcnt = at<uint32_t>(ws, L.fpcnt); fa.maxp = L.fmaxp;
     fa.cap = p->capacity; fa.out_count = b->counts; fa.out_dropped = b->dropped;
     fa.seg_stride = p->capacity;
     fa.out_t = b->ev_t; fa.out_x = b->ev_x; fa.out_y = b->ev_y; fa.out_p = b->ev_p;
@@ -232,6 +244,7 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
     mark(2);
     if (launch_fast_fix(fa, L.nseg, st) != cudaSuccess) return EVS_ERR_CUDA;
     if (launch_fast_redo(fa, L.nseg, st) != cudaSuccess) return EVS_ERR_CUDA;
+    if (launch_fast_plan(fa, L.nseg, st) != cudaSuccess) return EVS_ERR_CUDA;
     mark(3);
     if (launch_fast_order(fa, L.nseg, st) != cudaSuccess) return EVS_ERR_CUDA;
     mark(4);

@@ -115,6 +115,18 @@ struct LiteOut {
   float erel;  // relative band of j * uf
 };
 
+// Table of the lite log (shared memory): c_i, 1/c_i, log(c_i) (hi part).
+struct LiteTab {
+  double c[128], invc[128], lh[128];
+};
+__device__ __forceinline__ void load_lite_tab(LiteTab& t) {
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) {
+    t.c[i] = kLogTable[i][0];
+    t.invc[i] = kLogTable[i][1];
+    t.lh[i] = kLogTable[i][2];
+  }
+}
+
 // All roundings below are explicit (_rn intrinsics / fmaf) so that no FMA
 // contraction can differ between the passes that evaluate the same pixel
 // (K1's count pass, its emission pass, and k_fast_redo): the decisions must
@@ -122,7 +134,7 @@ struct LiteOut {
 //
 // Returns n (>= 0) or -1 when the exact path must decide.
 __device__ __forceinline__ int lite_count(float v, float r, float thp, float thn, float rthp, float rthn,
-                                          double log_eps, float dtf, bool& pos, LiteOut& o) {
+                                          double log_eps, float dtf, const LiteTab& T, bool& pos, LiteOut& o) {
   const double x = __dadd_rn((double)v, log_eps);  // the reference's x exactly
   const uint64_t ix = (uint64_t)__double_as_longlong(x);
   if (ix < 0x0010000000000000ull || ix >= 0x7ff0000000000000ull) return -1;
@@ -130,14 +142,14 @@ __device__ __forceinline__ int lite_count(float v, float r, float thp, float thn
   const int i = (int)((tmp >> (52 - kLogTableBits)) & ((1u << kLogTableBits) - 1));
   const int k = (int)((int64_t)tmp >> 52);
   const double z = __longlong_as_double((long long)(ix - (tmp & 0xfff0000000000000ull)));
-  const double d = __dsub_rn(z, kLogTable[i][0]);                       // exact
-  const float rf = __double2float_rn(__dmul_rn(d, kLogTable[i][1]));    // |r| <= 2^-7
+  const double d = __dsub_rn(z, T.c[i]);                               // exact
+  const float rf = __double2float_rn(__dmul_rn(d, T.invc[i]));          // |r| <= 2^-7
   float pf = fmaf(rf, 0.2f, -0.25f);
   pf = fmaf(pf, rf, 0.33333334f);
   pf = fmaf(pf, rf, -0.5f);
   pf = fmaf(pf, rf, 1.0f);
   pf = __fmul_rn(pf, rf);                                               // log1p(r), |err| < 2^-30
-  const double dd = __dsub_rn(fma((double)k, 0.6931471805599453, kLogTable[i][2]), (double)r);
+  const double dd = __dsub_rn(fma((double)k, 0.6931471805599453, T.lh[i]), (double)r);
   const float df = __fadd_rn(__double2float_rn(dd), pf);
   pos = df > 0.f;
   const float ad = fabsf(df);
@@ -179,13 +191,52 @@ struct PxStep {
   LiteOut lo;
 };
 
+// Exact path of one pixel-frame (rare; kept out of line so the hot loop stays small).
 template <bool REFR>
+__device__ __forceinline__ void exact_step(float v, float r, int lrel, float thp, float thn, const FrameCtx& c,
+                                        PxStep& o) {
+  double ad = 0.0, thd = 0.0;
+  const int n = exact_count(v, r, thp, thn, c.log_eps, o.pos, ad, thd);
+  int kept = 0, l = lrel;
+  for (int j = 1; j <= n; ++j) {
+    const int tr = exact_trel(j, thd, ad, c.dtd, c.dtm1);
+    if (REFR && c.tpr + tr - l < c.refr) continue;
+    l = c.tpr + tr;
+    ++kept;
+  }
+  o.n = n > 0 ? n : 0;
+  o.kept = kept;
+  o.lnew = l;
+  o.exact = true;
+}
+
+// Exact-path crossings of one pixel appended to a key list (rare path).
+template <bool REFR>
+__device__ __forceinline__ int exact_emit(float v, float rold, int lold, float thp, float thn, const FrameCtx& c,
+                                       uint32_t xyp, uint32_t* list, int off) {
+  double ad = 0.0, thd = 0.0;
+  bool pos;
+  const int n = exact_count(v, rold, thp, thn, c.log_eps, pos, ad, thd);
+  int l = lold;
+  for (int j = 1; j <= n; ++j) {
+    const int tr = exact_trel(j, thd, ad, c.dtd, c.dtm1);
+    if (REFR) {
+      if (c.tpr + tr - l < c.refr) continue;
+      l = c.tpr + tr;
+    }
+    list[off++] = ((uint32_t)tr << 12) | xyp;
+  }
+  return off;
+}
+
+template <bool REFR, bool PREF>
 __device__ __forceinline__ void px_step(float v, float r, int lrel, float thp, float thn, float rthp, float rthn,
-                                        const FrameCtx& c, PxStep& o) {
+                                        const FrameCtx& c, const LiteTab& T, PxStep& o) {
   o.n = 0;
   o.kept = 0;
   o.lnew = lrel;
-  {
+  o.exact = false;
+  if (PREF) {
     // f32 prefilter: |__logf - ln| <= 2^-21 |ln| + 2^-22 and the f32 rounding of
     // v + eps are far inside the margin, so a skipped pixel surely has n == 0
     const float lf = __logf(v + c.log_eps_f);
@@ -193,7 +244,7 @@ __device__ __forceinline__ void px_step(float v, float r, int lrel, float thp, f
     const float th32 = d32 > 0.f ? thp : thn;
     if (fabsf(d32) + (2e-6f * fabsf(lf) + 2e-6f) < th32 * (1.0f - 1e-4f)) return;
   }
-  int n = lite_count(v, r, thp, thn, rthp, rthn, c.log_eps, c.dtf, o.pos, o.lo);
+  int n = lite_count(v, r, thp, thn, rthp, rthn, c.log_eps, c.dtf, T, o.pos, o.lo);
   bool exact = n < 0;
   int kept = 0, l = lrel;
   if (!exact && n > 0) {
@@ -206,41 +257,79 @@ __device__ __forceinline__ void px_step(float v, float r, int lrel, float thp, f
     }
   }
   if (exact) {
-    double ad = 0.0, thd = 0.0;
-    n = exact_count(v, r, thp, thn, c.log_eps, o.pos, ad, thd);
-    kept = 0;
-    l = lrel;
-    for (int j = 1; j <= n; ++j) {
-      const int tr = exact_trel(j, thd, ad, c.dtd, c.dtm1);
-      if (REFR && c.tpr + tr - l < c.refr) continue;
-      l = c.tpr + tr;
-      ++kept;
-    }
+    exact_step<REFR>(v, r, lrel, thp, thn, c, o);
+    return;
   }
   o.n = n > 0 ? n : 0;
   o.kept = kept;
   o.lnew = l;
-  o.exact = exact;
 }
 
 // The kept crossing times of a pixel (chronological), as decided by px_step.
+// The kept crossings of a lite-path pixel (chronological), as px_step decided.
 template <bool REFR, typename Sink>
-__device__ __forceinline__ void px_emit(float v, float rold, int lold, float thp, float thn, int n, bool exact,
-                                        const LiteOut& lo, const FrameCtx& c, Sink&& sink) {
-  double ad = 0.0, thd = 0.0;
-  if (exact) {
-    bool p2;
-    exact_count(v, rold, thp, thn, c.log_eps, p2, ad, thd);
-  }
+__device__ __forceinline__ void px_emit(int lold, int n, const LiteOut& lo, const FrameCtx& c, Sink&& sink) {
   int l = lold;
   for (int j = 1; j <= n; ++j) {
-    const int tr = exact ? exact_trel(j, thd, ad, c.dtd, c.dtm1) : lite_trel(j, lo, c.dtm1);
+    // certified in px_step: floor(j*uf) lies inside the band, so it is the value
+    const int tr = min((int)floorf(__fmul_rn((float)j, lo.uf)), c.dtm1);
     if (REFR) {
       if (c.tpr + tr - l < c.refr) continue;
       l = c.tpr + tr;
     }
     sink(tr);
   }
+}
+
+// Straight-line lane math for the common case n <= 2 (no loops, no branches):
+// the same certified f32 evaluation as lite_count / lite_trel.  Returns
+//   bits 0-10 t_rel(1), 11-21 t_rel(2), 22 kept(1), 23 kept(2), 24 pos,
+//   25-26 n (0..2), 31 slow (band straddles an integer, n > 2, or x outside
+//   the table's range: px_step decides),
+// and the last kept time in lnew.  dt <= 2048 (11-bit t_rel).
+constexpr uint32_t kF2Slow = 0x80000000u, kF2K1 = 1u << 22, kF2K2 = 1u << 23, kF2Pos = 1u << 24;
+template <bool REFR>
+__device__ __forceinline__ uint32_t px_fast2(float v, float r, int lrel, float thp, float thn, float rthp,
+                                             float rthn, const FrameCtx& c, const LiteTab& T, int& lnew) {
+  const double x = __dadd_rn((double)v, c.log_eps);
+  const uint64_t ix = (uint64_t)__double_as_longlong(x);
+  const bool bad_x = ix < 0x0010000000000000ull || ix >= 0x7ff0000000000000ull;
+  const uint64_t tmp = ix - kLogOff;
+  const int i = (int)((tmp >> (52 - kLogTableBits)) & ((1u << kLogTableBits) - 1));
+  const int k = (int)((int64_t)tmp >> 52);
+  const double z = __longlong_as_double((long long)(ix - (tmp & 0xfff0000000000000ull)));
+  const double d = __dsub_rn(z, T.c[i]);
+  const float rf = __double2float_rn(__dmul_rn(d, T.invc[i]));
+  float pf = fmaf(rf, 0.2f, -0.25f);
+  pf = fmaf(pf, rf, 0.33333334f);
+  pf = fmaf(pf, rf, -0.5f);
+  pf = fmaf(pf, rf, 1.0f);
+  pf = __fmul_rn(pf, rf);
+  const double dd = __dsub_rn(fma((double)k, 0.6931471805599453, T.lh[i]), (double)r);
+  const float df = __fadd_rn(__double2float_rn(dd), pf);
+  const bool pos = df > 0.f;
+  const float ad = fabsf(df);
+  const float th = pos ? thp : thn;
+  const float rth = pos ? rthp : rthn;
+  const float q1 = fmaf(ad, rth, 1e-4f);
+  const float dn = fmaf(q1, 6e-7f, fmaf(1e-8f, rth, 1e-10f));
+  const float nlo = floorf(__fsub_rn(q1, dn)), nhi = floorf(__fadd_rn(q1, dn));
+  const int n = (int)nlo;
+  const float ra = rcp_approx(ad);
+  const float uf = __fmul_rn(__fmul_rn(th, c.dtf), ra);
+  const float erel = fmaf(1e-8f, ra, 1e-6f);
+  const float a1 = __fmul_rn(1.0f, uf), a2 = __fmul_rn(2.0f, uf);
+  const float b1 = fmaf(a1, erel, 1e-6f), b2 = fmaf(a2, erel, 1e-6f);
+  const int t1 = min((int)floorf(__fsub_rn(a1, b1)), c.dtm1), t1h = min((int)floorf(__fadd_rn(a1, b1)), c.dtm1);
+  const int t2 = min((int)floorf(__fsub_rn(a2, b2)), c.dtm1), t2h = min((int)floorf(__fadd_rn(a2, b2)), c.dtm1);
+  const bool slow = bad_x | (nlo != nhi) | (q1 > 1e6f) | (n > 2) | ((n >= 1) & (t1 != t1h)) |
+                    ((n >= 2) & (t2 != t2h));
+  const bool k1 = (n >= 1) && (!REFR || c.tpr + t1 - lrel >= c.refr);
+  const int l1 = k1 ? c.tpr + t1 : lrel;
+  const bool k2 = (n >= 2) && (!REFR || c.tpr + t2 - l1 >= c.refr);
+  lnew = k2 ? c.tpr + t2 : l1;
+  return (slow ? kF2Slow : 0u) | ((uint32_t)(t1 & 0x7ff)) | ((uint32_t)(t2 & 0x7ff) << 11) | (k1 ? kF2K1 : 0u) |
+         (k2 ? kF2K2 : 0u) | (pos ? kF2Pos : 0u) | ((uint32_t)(n & 3) << 25);
 }
 
 // ---------------------------------------------------------------------------
@@ -271,19 +360,17 @@ __device__ __forceinline__ int clamp_rel(int64_t d) {
 
 template <bool REFR, bool UNI>
 __global__ void __launch_bounds__(kFNT, 2) k_fast_gen(FastArgs a) {
-  constexpr int NT = kFNT, VPT = kFVpt, NW = NT / 32, KB = kFMaxBuckets;
+  constexpr int NT = kFNT, VPT = kFVpt, NW = NT / 32, KB = kFMaxBuckets, WCAP = kFListCap / NW;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* s_list = reinterpret_cast<uint32_t*>(smem_raw);  // [kFListCap] pixel-major keys
-  uint32_t* s_sorted = s_list + kFListCap;                     // [kFListCap] bucket-sorted keys
+  uint32_t* s_list = reinterpret_cast<uint32_t*>(smem_raw);  // [NW][WCAP] pixel-major keys per warp
+  uint32_t* s_sorted = s_list + kFListCap;                     // [kFListCap] bucket-sorted keys of the tile
   uint32_t* s_wcnt = s_sorted + kFListCap;                     // [NW][KB] per-warp bucket counters
-  float* s_uf = reinterpret_cast<float*>(s_wcnt + NW * KB);    // [kFGmax] per-pixel carry to the emission:
-  float* s_erel = s_uf + kFGmax;                               //   lite step and band
-  int* s_meta = reinterpret_cast<int*>(s_erel + kFGmax);       //   n | exact << 24
-  int* s_lold = s_meta + kFGmax;                               //   last event before the frame
-  float* s_rold = reinterpret_cast<float*>(s_lold + kFGmax);   //   level before the frame
+  __shared__ LiteTab s_tab;
   __shared__ uint32_t s_bstart[KB + 1];
-  __shared__ int s_scan[NW + 1];
-  __shared__ uint32_t s_res2[2];  // per frame parity (read + reset without a trailing barrier)
+  __shared__ uint32_t s_wtot[KB / 32];
+  __shared__ int s_wn[NW];         // crossings per warp (this frame)
+  __shared__ uint32_t s_res2[2];   // reservation chunks, per frame parity
+  __shared__ int s_ovf2[2];        // a warp list overflowed, per frame parity
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s = blockIdx.x / a.ntiles;
@@ -299,6 +386,7 @@ __global__ void __launch_bounds__(kFNT, 2) k_fast_gen(FastArgs a) {
   const int64_t t0c = a.desc ? a.desc->cur_t0 : a.t0;
   const int64_t tb = frame_tprev(a, s, 0, t0c);  // time base of the relative times
   const int nbk = a.nbk;
+  uint32_t* wlist = s_list + warp * WCAP;
 
   // ---- state into registers ----
   float r[VPT], thp[VPT], thn[VPT], rthp[VPT], rthn[VPT];
@@ -347,7 +435,8 @@ __global__ void __launch_bounds__(kFNT, 2) k_fast_gen(FastArgs a) {
     }
   }
   for (int i = tid; i < NW * KB; i += NT) s_wcnt[i] = 0;
-  if (tid < 2) s_res2[tid] = 0;
+  if (tid < 2) { s_res2[tid] = 0; s_ovf2[tid] = 0; }
+  load_lite_tab(s_tab);
 
   auto load_frame = [&](int f, float* dst) {
     const float* fr = a.frames + ((int64_t)s * a.T + f) * P;
@@ -365,123 +454,166 @@ __global__ void __launch_bounds__(kFNT, 2) k_fast_gen(FastArgs a) {
 
   for (int f = 0; f < a.T; ++f) {
     const int seg = s * a.T + f;
+    const int64_t st_idx = (int64_t)seg * a.ntiles + tile;
     const FrameCtx c = frame_ctx(a, s, f, t0c, tb);
     uint32_t& s_res = s_res2[f & 1];
+    int& s_ovf = s_ovf2[f & 1];
     float v[VPT];
 #pragma unroll
     for (int k = 0; k < VPT; ++k) v[k] = vnext[k];
     if (f + 1 < a.T) load_frame(f + 1, vnext);
 
-    // ---- 1. lane math: crossings, refractory, new state ----
-    uint32_t emask = 0;  // bit k: pixel k has kept crossings; bit 4+k: its level changed
+    // ---- 1. lane math (registers): crossings, refractory filter, new state ----
+    float rnew[VPT];
+    int lnew[VPT];
+    uint32_t pk[VPT];  // px_fast2 result (kF2Slow: px_step decides, again at emission)
     int cnt = 0;
+    uint32_t chg = 0;  // bit k: level changes, bit 4+k: kept crossings
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
-      if (lp0 + k >= gt) continue;
-      PxStep o;
-      px_step<REFR>(v[k], r[k], lrel[k], thp[k], thn[k], rthp[k], rthn[k], c, o);
-      if (o.n == 0) continue;
-      const int lp = lp0 + k;
-      s_rold[lp] = r[k];
-      s_lold[lp] = lrel[k];
-      // new level f32(ls +- n*th) (model.py:159-162); n*th is exact in f64
-      const double step = __dmul_rn((double)o.n, (double)(o.pos ? thp[k] : thn[k]));
-      r[k] = __double2float_rn(o.pos ? __dadd_rn((double)r[k], step) : __dsub_rn((double)r[k], step));
-      dirty |= 1u << k;
-      emask |= 16u << k;
-      if (o.kept > 0) {
-        lrel[k] = o.lnew;
-        dirty |= 16u << k;
-        emask |= 1u << k;
-        s_uf[lp] = o.lo.uf;
-        s_erel[lp] = o.lo.erel;
-        s_meta[lp] = min(o.n, 0x7fffff) | (o.pos ? (1 << 23) : 0) | (o.exact ? (1 << 24) : 0);
+      pk[k] = 0; rnew[k] = r[k]; lnew[k] = lrel[k];
+      if (!full && lp0 + k >= gt) continue;
+      int ln;
+      uint32_t res = px_fast2<REFR>(v[k], r[k], lrel[k], thp[k], thn[k], rthp[k], rthn[k], c, s_tab, ln);
+      int n, kept;
+      bool pos;
+      if (res & kF2Slow) {
+        PxStep o;
+        px_step<REFR, false>(v[k], r[k], lrel[k], thp[k], thn[k], rthp[k], rthn[k], c, s_tab, o);
+        n = o.n; kept = o.kept; pos = o.pos; ln = o.lnew;
+        res = kF2Slow;
+      } else {
+        n = (int)((res >> 25) & 3u);
+        kept = (int)((res >> 22) & 1u) + (int)((res >> 23) & 1u);
+        pos = (res & kF2Pos) != 0;
       }
-      cnt += o.kept;
+      pk[k] = kept > 0 ? res : 0u;
+      // new level f32(ls +- n*th) (model.py:159-162); n*th is exact in f64 (n = 0: unchanged)
+      const double step = __dmul_rn((double)n, (double)(pos ? thp[k] : thn[k]));
+      rnew[k] = __double2float_rn(pos ? __dadd_rn((double)r[k], step) : __dsub_rn((double)r[k], step));
+      chg |= (n > 0 ? 1u : 0u) << k;
+      if (kept > 0) { chg |= 16u << k; lnew[k] = ln; }
+      cnt += kept;
     }
-    // 32-pixel chunks with >= 1 kept event (AggregationStats.reservation_count):
-    // a chunk is 8 consecutive lanes; tiles start on chunk boundaries
+    // ---- 2. warp-local pixel-major emission + per-warp bucket histogram ----
+    int off = warp_incl_scan(cnt);
+    const int wn = __shfl_sync(0xffffffffu, off, 31);
+    off -= cnt;
     {
+      // 32-pixel chunks with >= 1 kept event (AggregationStats.reservation_count):
+      // a chunk is 8 consecutive lanes; tiles start on chunk boundaries
       const uint32_t b = __ballot_sync(0xffffffffu, cnt > 0);
-      if (lane == 0 && b) {
-        const uint32_t cc = ((b & 0xffu) != 0) + ((b & 0xff00u) != 0) + ((b & 0xff0000u) != 0) +
-                            ((b & 0xff000000u) != 0);
-        atomicAdd(&s_res, cc);
+      if (lane == 0) {
+        s_wn[warp] = wn;
+        if (b) {
+          const uint32_t cc = ((b & 0xffu) != 0) + ((b & 0xff00u) != 0) + ((b & 0xff0000u) != 0) +
+                              ((b & 0xff000000u) != 0);
+          atomicAdd(&s_res, cc);
+        }
+        if (wn > WCAP) s_ovf = 1;
       }
     }
-    // ---- 2. pixel-major compaction ----
-    int total;
-    int off = block_excl_scan<NT, int>(cnt, s_scan, &total);
-    const int wbeg = __shfl_sync(0xffffffffu, off, 0);
-    const int wend = __shfl_sync(0xffffffffu, off + cnt, 31);
-    const int64_t st_idx = (int64_t)seg * a.ntiles + tile;
-    if (total > kFListCap) {  // block-uniform, rare: k_fast_redo regenerates this tile-frame
+    if (wn <= WCAP && cnt > 0) {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        const uint32_t res = pk[k];
+        if (res == 0) continue;
+        const uint32_t xy = (uint32_t)(lp0 + k) << 1;
+        if (!(res & kF2Slow)) {
+          const uint32_t xyp = xy | ((res & kF2Pos) ? 1u : 0u);
+          if (res & kF2K1) wlist[off++] = ((res & 0x7ffu) << 12) | xyp;
+          if (res & kF2K2) wlist[off++] = (((res >> 11) & 0x7ffu) << 12) | xyp;
+        } else {
+          PxStep o;
+          px_step<REFR, false>(v[k], r[k], lrel[k], thp[k], thn[k], rthp[k], rthn[k], c, s_tab, o);
+          const uint32_t xyp = xy | (o.pos ? 1u : 0u);
+          if (o.exact)
+            off = exact_emit<REFR>(v[k], r[k], lrel[k], thp[k], thn[k], c, xyp, wlist, off);
+          else
+            px_emit<REFR>(lrel[k], o.n, o.lo, c, [&](int tr) { wlist[off++] = ((uint32_t)tr << 12) | xyp; });
+        }
+      }
+    }
+    __syncwarp();
+    if (wn <= WCAP) {  // per-warp bucket counts (warp-aggregated: one smem update per bucket group)
+      for (int base = 0; base < wn; base += 32) {
+        const int i = base + lane;
+        const bool valid = i < wn;
+        const uint32_t active = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+          const int bk = (int)(wlist[i] >> 15);
+          const uint32_t peers = __match_any_sync(active, bk);
+          if (lane == __ffs(peers) - 1) s_wcnt[warp * KB + bk] += __popc(peers);
+        }
+      }
+    }
+    __syncthreads();  // A
+    if (s_ovf) {  // block-uniform, rare: k_fast_redo regenerates this tile-frame
       float* sr = a.snap_ref + st_idx * a.G;
       int* sl = a.snap_last + st_idx * a.G;
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
-        const int lp = lp0 + k;
-        if (lp >= gt) continue;
-        const bool ch = (emask >> (4 + k)) & 1u;
-        sr[lp] = ch ? s_rold[lp] : r[k];
-        sl[lp] = ch ? s_lold[lp] : lrel[k];
+        if (lp0 + k >= gt) continue;
+        sr[lp0 + k] = r[k];
+        sl[lp0 + k] = lrel[k];
+        r[k] = rnew[k];
+        lrel[k] = lnew[k];
       }
-      __syncthreads();
+      dirty |= chg;
+      for (int i = tid; i < NW * KB; i += NT) s_wcnt[i] = 0;
       if (tid == 0) {
+        int total = 0;
+        for (int w = 0; w < NW; ++w) total += s_wn[w];
         a.tile_src[st_idx] = kSrcRedo;
         a.rows[((int64_t)seg * (nbk + 1) + nbk) * a.ntiles + tile] = (uint32_t)total;
         if (s_res) atomicAdd(reinterpret_cast<unsigned long long*>(a.seg_res + seg), (unsigned long long)s_res);
         s_res = 0;
       }
-      __syncthreads();
+      __syncthreads();  // everyone has read s_ovf; counters are zero again
+      if (tid == 0) s_ovf = 0;  // (this parity slot is next used by frame f + 2)
       continue;
     }
-    if (emask & 0xfu) {
 #pragma unroll
-      for (int k = 0; k < VPT; ++k) {
-        if (!((emask >> k) & 1u)) continue;
-        const int lp = lp0 + k;
-        const int meta = s_meta[lp];
-        const uint32_t xyp = ((uint32_t)lp << 1) | ((meta >> 23) & 1u);
-        const LiteOut lo{s_uf[lp], s_erel[lp]};
-        px_emit<REFR>(v[k], s_rold[lp], s_lold[lp], thp[k], thn[k], meta & 0x7fffff, (meta >> 24) & 1, lo, c,
-                      [&](int tr) {
-                        s_list[off++] = ((uint32_t)tr << 12) | xyp;
-                        atomicAdd(&s_wcnt[warp * KB + (tr >> 3)], 1u);
-                      });
+    for (int k = 0; k < VPT; ++k) {  // apply the new state
+      r[k] = rnew[k];
+      lrel[k] = lnew[k];
+    }
+    dirty |= chg;
+
+    // ---- 3. bucket starts: column prefix over warps, scan over buckets ----
+    uint32_t tot = 0;
+    if (tid < nbk) {
+#pragma unroll 4
+      for (int w = 0; w < NW; ++w) {
+        const uint32_t cc = s_wcnt[w * KB + tid];
+        s_wcnt[w * KB + tid] = tot;
+        tot += cc;
       }
     }
-    __syncthreads();
-
-    // ---- 3. bucket starts: column prefix over warps, exclusive scan over buckets ----
-    {
-      uint32_t tot = 0;
-      if (tid < nbk) {
+    uint32_t inc = warp_incl_scan(tot);
+    if (lane == 31 && warp < KB / 32) s_wtot[warp] = inc;
+    __syncthreads();  // B
+    int total = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) total += s_wn[w];
+    if (tid < nbk) {
+      uint32_t wb = 0;
+      for (int w = 0; w < warp; ++w) wb += s_wtot[w];
+      const uint32_t bst = wb + inc - tot;
 #pragma unroll 4
-        for (int w = 0; w < NW; ++w) {
-          const uint32_t cc = s_wcnt[w * KB + tid];
-          s_wcnt[w * KB + tid] = tot;
-          tot += cc;
-        }
-      }
-      int tt;
-      const uint32_t bst = (uint32_t)block_excl_scan<NT, int>((int)tot, s_scan, &tt);
-      if (tid < nbk) {
-#pragma unroll 4
-        for (int w = 0; w < NW; ++w) s_wcnt[w * KB + tid] += bst;
-        s_bstart[tid] = bst;
-      }
-      if (tid == 0) s_bstart[nbk] = (uint32_t)total;
+      for (int w = 0; w < NW; ++w) s_wcnt[w * KB + tid] += bst;
+      s_bstart[tid] = bst;
     }
-    __syncthreads();
+    if (tid == 0) s_bstart[nbk] = (uint32_t)total;
+    __syncthreads();  // C
 
-    // ---- 4. stable rank (warp match-any, pixel order) and scatter ----
-    for (int base = wbeg; base < wend; base += 32) {
+    // ---- 4. stable rank (warp match-any over the warp's list, pixel order) ----
+    for (int base = 0; base < wn; base += 32) {
       const int i = base + lane;
-      const bool valid = i < wend;
+      const bool valid = i < wn;
       const uint32_t active = __ballot_sync(0xffffffffu, valid);
       if (valid) {
-        const uint32_t key = s_list[i];
+        const uint32_t key = wlist[i];
         const int bk = (int)(key >> 15);
         const uint32_t peers = __match_any_sync(active, bk);
         const int leader = __ffs(peers) - 1;
@@ -494,7 +626,7 @@ __global__ void __launch_bounds__(kFNT, 2) k_fast_gen(FastArgs a) {
         s_sorted[bpos + __popc(peers & lanemask_lt())] = key;
       }
     }
-    __syncthreads();
+    __syncthreads();  // D
 
     // ---- 5. sorted keys and bucket starts out; reset the counters ----
     {
@@ -505,7 +637,12 @@ __global__ void __launch_bounds__(kFNT, 2) k_fast_gen(FastArgs a) {
       for (int i = 4 * n4 + tid; i < total; i += NT) dst[i] = s_sorted[i];
       uint32_t* rows = a.rows + (int64_t)seg * (nbk + 1) * a.ntiles + tile;
       for (int b = tid; b <= nbk; b += NT) rows[(int64_t)b * a.ntiles] = s_bstart[b];
-      for (int i = tid; i < NW * KB; i += NT) s_wcnt[i] = 0;
+      if (tid < nbk) {
+#pragma unroll 4
+        for (int w = 0; w < NW; ++w) s_wcnt[w * KB + tid] = 0;
+        const uint32_t cb = s_bstart[tid + 1] - s_bstart[tid];
+        if (cb) atomicAdd(a.btot + (int64_t)seg * nbk + tid, cb);
+      }
       if (tid == 0) {
         a.tile_src[st_idx] = kSrcSlot;
         if (s_res) atomicAdd(reinterpret_cast<unsigned long long*>(a.seg_res + seg), (unsigned long long)s_res);
@@ -642,6 +779,13 @@ __global__ void __launch_bounds__(kFixNT) k_fast_fix(FastArgs a) {
       if (tid < nbk) rows[(int64_t)tid * nt + qc] = (uint32_t)ex;
       if (tid == 0) rows[(int64_t)nbk * nt + qc] = (uint32_t)tt;
     }
+    __syncthreads();
+    for (int k = tid; k < nbk; k += NT) {
+      uint32_t acc = 0;
+      for (int q = 0; q < nt; ++q)
+        if (src[q] != kSrcRedo) acc += rows[(int64_t)(k + 1) * nt + q] - rows[(int64_t)k * nt + q];
+      a.btot[(int64_t)seg * nbk + k] = acc;
+    }
   }
   if (tid == 0) {
     const int64_t written = total < cap ? total : cap;
@@ -663,9 +807,13 @@ __global__ void __launch_bounds__(kRedoNT) k_fast_redo(FastArgs a) {
   constexpr int NT = kRedoNT, PPT = (kFGmax + NT - 1) / NT;
   __shared__ int s_scan[NT / 32 + 1];
   __shared__ uint32_t s_hist[kFMaxBuckets + 1];
+  __shared__ LiteTab s_tab;
   const int seg = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
   if (*a.bad != kNoBad) return;
   const int nitems = a.redo_n[seg];
+  if (blockIdx.x >= nitems) return;
+  load_lite_tab(s_tab);
+  __syncthreads();
   const int s = seg / a.T, f = seg % a.T;
   const int nbk = a.nbk, nt = a.ntiles;
   const int64_t t0c = a.desc ? a.desc->cur_t0 : a.t0;
@@ -695,7 +843,7 @@ __global__ void __launch_bounds__(kRedoNT) k_fast_redo(FastArgs a) {
       const float thp = tp ? tp[lp] : a.thp_u, thn = tn ? tn[lp] : a.thn_u;
       const float rthp = tp ? __frcp_rn(thp) : a.rthp_u, rthn = tn ? __frcp_rn(thn) : a.rthn_u;
       PxStep o;
-      px_step<REFR>(fr[lp], sr[lp], sl[lp], thp, thn, rthp, rthn, c, o);
+      px_step<REFR, kFPrefilter>(fr[lp], sr[lp], sl[lp], thp, thn, rthp, rthn, c, s_tab, o);
       cnt += o.kept;
     }
     int total;
@@ -706,13 +854,30 @@ __global__ void __launch_bounds__(kRedoNT) k_fast_redo(FastArgs a) {
       const float thp = tp ? tp[lp] : a.thp_u, thn = tn ? tn[lp] : a.thn_u;
       const float rthp = tp ? __frcp_rn(thp) : a.rthp_u, rthn = tn ? __frcp_rn(thn) : a.rthn_u;
       PxStep o;
-      px_step<REFR>(fr[lp], sr[lp], sl[lp], thp, thn, rthp, rthn, c, o);
+      px_step<REFR, kFPrefilter>(fr[lp], sr[lp], sl[lp], thp, thn, rthp, rthn, c, s_tab, o);
       if (o.kept == 0) continue;
       const uint32_t xyp = ((uint32_t)lp << 1) | (o.pos ? 1u : 0u);
-      px_emit<REFR>(fr[lp], sr[lp], sl[lp], thp, thn, o.n, o.exact, o.lo, c, [&](int tr) {
-        if (off < lim) un[off] = ((uint32_t)tr << 12) | xyp;
-        ++off;
-      });
+      if (o.exact) {
+        // regenerate into a small local buffer-free path: count, then write those below lim
+        double ad = 0.0, thd = 0.0;
+        bool p2;
+        const int n = exact_count(fr[lp], sr[lp], thp, thn, c.log_eps, p2, ad, thd);
+        int l = sl[lp];
+        for (int j = 1; j <= n; ++j) {
+          const int tr = exact_trel(j, thd, ad, c.dtd, c.dtm1);
+          if (REFR) {
+            if (c.tpr + tr - l < c.refr) continue;
+            l = c.tpr + tr;
+          }
+          if (off < lim) un[off] = ((uint32_t)tr << 12) | xyp;
+          ++off;
+        }
+      } else {
+        px_emit<REFR>(sl[lp], o.n, o.lo, c, [&](int tr) {
+          if (off < lim) un[off] = ((uint32_t)tr << 12) | xyp;
+          ++off;
+        });
+      }
     }
     for (int b = tid; b <= nbk; b += NT) s_hist[b] = 0;
     __syncthreads();
@@ -722,7 +887,11 @@ __global__ void __launch_bounds__(kRedoNT) k_fast_redo(FastArgs a) {
       const int cc = tid < nbk ? (int)s_hist[tid] : 0;
       int tt;
       const int ex = block_excl_scan<NT, int>(cc, s_scan, &tt);
-      if (tid < nbk) { s_hist[tid] = (uint32_t)ex; rows[(int64_t)tid * nt + q] = (uint32_t)ex; }
+      if (tid < nbk) {
+        if (cc) atomicAdd(a.btot + (int64_t)seg * nbk + tid, (uint32_t)cc);
+        s_hist[tid] = (uint32_t)ex;
+        rows[(int64_t)tid * nt + q] = (uint32_t)ex;
+      }
       if (tid == 0) rows[(int64_t)nbk * nt + q] = (uint32_t)lim;
     }
     __syncthreads();
@@ -752,39 +921,134 @@ __global__ void __launch_bounds__(kRedoNT) k_fast_redo(FastArgs a) {
 // ---------------------------------------------------------------------------
 // K2: one CTA per (segment, bucket of 8 t_rel bins)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void bucket_place(const uint32_t* in, uint32_t* out, int n, int* binstart,
-                                             uint32_t* bintot, uint64_t* s_scan64) {
-  // stable counting sort of in[0..n) by bits 25-27 (t_rel within the bucket)
+// Gather entry: pixel (24 bits) | p << 24 | (t_rel & 7) << 25.
+__device__ __forceinline__ uint32_t gentry(uint32_t key, uint32_t gpx0) {
+  return (gpx0 + ((key >> 1) & 0x7ffu)) | ((key & 1u) << 24) | (((key >> 12) & 7u) << 25);
+}
+
+// Per-warp bin counts of s_g[lo, hi) (lane v < 8 returns the count of bin v).
+__device__ __forceinline__ uint32_t warp_bin_counts(const uint32_t* s_g, int lo, int hi) {
+  const int lane = threadIdx.x & 31;
+  uint32_t my = 0;
+  for (int base = lo; base < hi; base += 32) {
+    const int i = base + lane;
+    const uint32_t b = i < hi ? (s_g[i] >> 25) & 7u : 8u;
+#pragma unroll
+    for (uint32_t v = 0; v < 8; ++v) {
+      const uint32_t m = __ballot_sync(0xffffffffu, b == v);
+      if (lane == (int)v) my += __popc(m);
+    }
+  }
+  return my;
+}
+
+// plan (one CTA per segment): split the buckets into pieces of about kOCap
+// events.  A bucket above kOCap ("big") is cut at tile boundaries; its pieces
+// get per-bin counts from k_fast_count so each can place its events.
+constexpr int kPlanNT = 256;
+__global__ void __launch_bounds__(kPlanNT) k_fast_plan(FastArgs a) {
+  constexpr int NT = kPlanNT;
+  __shared__ int s_len[kFMaxTiles];
+  __shared__ uint32_t s_bt[kFMaxBuckets];
+  __shared__ int s_scan[NT / 32 + 1];
+  __shared__ int s_np;
+  const int seg = blockIdx.x, tid = threadIdx.x;
+  const int nbk = a.nbk, nt = a.ntiles;
+  const uint32_t* rows = a.rows + (int64_t)seg * (nbk + 1) * nt;
+  int* pc = a.pieces + (int64_t)seg * a.maxp * 8;
+  for (int k = tid; k < nbk; k += NT) s_bt[k] = a.btot[(int64_t)seg * nbk + k];
+  __syncthreads();
+  // small buckets (<= kOCap events): one piece each, written in parallel
+  {
+    int run = 0;
+    for (int k0 = 0; k0 < nbk; k0 += NT) {
+      const int k = k0 + tid;
+      const bool small = k < nbk && s_bt[k] > 0 && s_bt[k] <= (uint32_t)kOCap;
+      int tt;
+      const int ex = run + block_excl_scan<NT, int>(small ? 1 : 0, s_scan, &tt);
+      if (small) {
+        int* e = pc + ex * 8;
+        e[0] = k; e[1] = 0; e[2] = nt; e[3] = ex; e[4] = ex + 1; e[5] = 0;
+      }
+      run += tt;
+    }
+    if (tid == 0) s_np = run;
+    __syncthreads();
+  }
+  for (int k = 0; k < nbk; ++k) {
+    if (s_bt[k] <= (uint32_t)kOCap) continue;  // (uniform)
+    // big bucket: a piece starts where floor(prefix / kSplit) advances (tile
+    // granularity, so a piece holds <= kSplit + one slice; k_fast_order walks a
+    // piece larger than kOCap in chunks)
+    constexpr int kSplit = kOCap - 1024;
+    const int j0 = s_np;
+    for (int q = tid; q < nt; q += NT)
+      s_len[q] = (int)(rows[(int64_t)(k + 1) * nt + q] - rows[(int64_t)k * nt + q]);
+    __syncthreads();
+    int run = 0, nb = 0;
+    for (int q0 = 0; q0 < nt; q0 += NT) {
+      const int q = q0 + tid;
+      const int len = q < nt ? s_len[q] : 0;
+      int tt;
+      const int pre = run + block_excl_scan<NT, int>(len, s_scan, &tt);
+      const int plen = (q > 0 && q < nt) ? s_len[q - 1] : 0;  // tile q-1 starts at pre - plen
+      const bool start = q < nt && (q == 0 || (pre / kSplit) != ((pre - plen) / kSplit));
+      int ns;
+      const int ex = nb + block_excl_scan<NT, int>(start ? 1 : 0, s_scan, &ns);
+      if (start) {
+        int* e = pc + (j0 + ex) * 8;
+        e[0] = k; e[1] = q; e[3] = j0; e[5] = 1;
+      }
+      run += tt;
+      nb += ns;
+    }
+    __syncthreads();
+    for (int jj = j0 + tid; jj < j0 + nb; jj += NT) {
+      int* e = pc + jj * 8;
+      e[2] = jj + 1 < j0 + nb ? pc[(jj + 1) * 8 + 1] : nt;
+      e[4] = j0 + nb;
+    }
+    __syncthreads();
+    if (tid == 0) s_np = j0 + nb;
+    __syncthreads();
+  }
+  if (tid == 0) a.npieces[seg] = s_np;
+}
+
+// per-bin counts of every piece of a big bucket
+__global__ void __launch_bounds__(kONT) k_fast_count(FastArgs a) {
   constexpr int NT = kONT;
-  const int tid = threadIdx.x;
-  const int m = (n + NT - 1) / NT;
-  const int i0 = min(n, tid * m), i1 = min(n, i0 + m);
-  uint64_t lo = 0, hi = 0;  // 8 x 16-bit counters
-  for (int i = i0; i < i1; ++i) {
-    const uint32_t b = (in[i] >> 25) & 7u;
-    if (b < 4) lo += 1ull << (16 * b); else hi += 1ull << (16 * (b - 4));
-  }
-  uint64_t tlo, thi;
-  const uint64_t plo = block_excl_scan<NT, uint64_t>(lo, s_scan64, &tlo);
-  const uint64_t phi = block_excl_scan<NT, uint64_t>(hi, s_scan64, &thi);
-  uint32_t st[8];
-  uint32_t acc = 0;
+  __shared__ uint32_t s_c[8];
+  const int seg = blockIdx.y, tid = threadIdx.x;
+  if (*a.bad != kNoBad) return;
+  const int np = a.npieces[seg];
+  const int nbk = a.nbk, nt = a.ntiles;
+  const uint32_t* rows = a.rows + (int64_t)seg * (nbk + 1) * nt;
+  for (int j = blockIdx.x; j < np; j += gridDim.x) {
+    const int* e = a.pieces + ((int64_t)seg * a.maxp + j) * 8;
+    if (!e[5]) continue;
+    const int k = e[0], qa = e[1], qb = e[2];
+    if (tid < 8) s_c[tid] = 0;
+    __syncthreads();
+    uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int q = qa + tid; q < qb; q += NT) {
+      const uint32_t s0 = rows[(int64_t)k * nt + q], s1 = rows[(int64_t)(k + 1) * nt + q];
+      if (s1 == s0) continue;
+      const uint32_t* src = tile_keys(a, seg, q);
+      for (uint32_t i = s0; i < s1; ++i) {
+        const uint32_t b = (__ldg(src + i) >> 12) & 7u;
 #pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    const uint32_t t = (uint32_t)(((b < 4 ? tlo : thi) >> (16 * (b & 3))) & 0xffffu);
-    st[b] = acc + (uint32_t)(((b < 4 ? plo : phi) >> (16 * (b & 3))) & 0xffffu);
-    if (tid == 0) { binstart[b] = (int)acc; bintot[b] = t; }
-    acc += t;
-  }
-  for (int i = i0; i < i1; ++i) {
-    const uint32_t e = in[i];
-    const uint32_t b = (e >> 25) & 7u;
-    uint32_t pos = st[0];
+        for (int v = 0; v < 8; ++v) c[v] += b == (uint32_t)v;
+      }
+    }
 #pragma unroll
-    for (int cc = 1; cc < 8; ++cc) pos = b == (uint32_t)cc ? st[cc] : pos;
-    out[pos] = e;
-#pragma unroll
-    for (int cc = 0; cc < 8; ++cc) st[cc] += b == (uint32_t)cc ? 1u : 0u;
+    for (int v = 0; v < 8; ++v) {
+      const uint32_t w = warp_sum(c[v]);
+      if ((tid & 31) == 0 && w) atomicAdd(&s_c[v], w);
+    }
+    __syncthreads();
+    if (tid < 8) a.pcnt[((int64_t)seg * a.maxp + j) * 8 + tid] = s_c[tid];
+    __syncthreads();
   }
 }
 
@@ -793,110 +1057,170 @@ __global__ void __launch_bounds__(kONT, 2) k_fast_order(FastArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* s_g = reinterpret_cast<uint32_t*>(smem_raw);  // [kOCap] gathered entries
   uint32_t* s_s = s_g + kOCap;                             // [kOCap] bin-sorted entries
-  int* s_goff = reinterpret_cast<int*>(s_s + kOCap);       // [ntiles + 1]
-  int* s_s0 = s_goff + a.ntiles + 1;                       // [ntiles]
-  __shared__ uint64_t s_scan64[NW + 1];
-  __shared__ int64_t s_red[NW + 1];
+  int* s_goff = reinterpret_cast<int*>(s_s + kOCap);       // [ntiles + 1] gather offsets
+  uint32_t* s_src = reinterpret_cast<uint32_t*>(s_goff + a.ntiles + 1);  // [ntiles] slice start
   __shared__ int s_scan[NW + 1];
-  __shared__ int s_binstart[8];
-  __shared__ uint32_t s_bintot[8];
-  __shared__ int64_t s_gbs[8];
-  __shared__ int64_t s_grun[8];
-  __shared__ uint32_t s_cnt[8];
+  __shared__ uint32_t s_wc[NW][8];   // per-warp bin counts -> per-warp bin offsets
+  __shared__ uint32_t s_cbs[9];      // bin starts within the chunk (+ total)
+  __shared__ int64_t s_pbs[8];       // bin starts of this piece's events within the bucket
+  __shared__ int64_t s_kbase[kFMaxBuckets + 1];  // bucket bases within the segment
 
-  const int seg = blockIdx.y, k = blockIdx.x, tid = threadIdx.x;
+  const int seg = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (*a.bad != kNoBad) return;
+  const int np = a.npieces[seg];
+  if ((int)blockIdx.x >= np) return;
   const int nbk = a.nbk, nt = a.ntiles;
   const int s = seg / a.T, f = seg % a.T;
   const uint32_t* rows = a.rows + (int64_t)seg * (nbk + 1) * nt;
   const int64_t t0c = a.desc ? a.desc->cur_t0 : a.t0;
-  const int64_t tbin0 = frame_tprev(a, s, f, t0c) + 8 * k;
-
-  // slice of every tile, gather offsets, and the bucket's base in the segment
-  int64_t base_part = 0;
-  int run = 0;
-  for (int q0 = 0; q0 < nt; q0 += NT) {
-    const int q = q0 + tid;
-    int len = 0;
-    if (q < nt) {
-      const uint32_t s0 = rows[(int64_t)k * nt + q];
-      const uint32_t s1 = rows[(int64_t)(k + 1) * nt + q];
-      s_s0[q] = (int)s0;
-      len = (int)(s1 - s0);
-      base_part += s0;
-    }
+  const int64_t tprev = frame_tprev(a, s, f, t0c);
+  const uint32_t* keys_seg = a.keys + (int64_t)seg * nt * kFListCap;
+  const uint32_t* area_seg = a.area_sorted + (int64_t)seg * a.cap;
+  {
+    // bucket bases: exclusive scan of the bucket totals
+    const uint32_t* bt = a.btot + (int64_t)seg * nbk;
     int tt;
-    const int ex = block_excl_scan<NT, int>(len, s_scan, &tt);
-    if (q < nt) s_goff[q] = run + ex;
-    run += tt;
-  }
-  const int total = run;
-  if (tid == 0) s_goff[nt] = total;
-  int64_t base;
-  block_excl_scan<NT, int64_t>(base_part, s_red, &base);  // (syncs)
-  if (total == 0) return;
-  const int64_t ob = (int64_t)seg * a.seg_stride + base;
-  const bool multi = total > kOCap;
-  if (multi) {
-    // pass A: bin totals of the whole bucket
-    if (tid < 8) s_cnt[tid] = 0;
-    __syncthreads();
-    for (int q = tid >> 3; q < nt; q += NT / 8) {
-      const int len = s_goff[q + 1] - s_goff[q];
-      const uint32_t* srcp = tile_keys(a, seg, q) + s_s0[q];
-      for (int j = tid & 7; j < len; j += 8) atomicAdd(&s_cnt[(srcp[j] >> 12) & 7u], 1u);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int64_t acc = 0;
-      for (int b = 0; b < 8; ++b) { s_gbs[b] = acc; s_grun[b] = 0; acc += s_cnt[b]; }
-    }
+    const int c = tid < nbk ? (int)bt[tid] : 0;
+    const int ex = block_excl_scan<NT, int>(c, s_scan, &tt);
+    if (tid < nbk) s_kbase[tid] = ex;
+    if (tid == 0) s_kbase[nbk] = tt;
     __syncthreads();
   }
   const int W = a.W;
   const float winv = 1.0f / (float)W;
-  for (int g0 = 0; g0 < total; g0 += kOCap) {
-    const int n = min(kOCap, total - g0);
-    // gather: 8 lanes per tile, tiles overlapping [g0, g0 + n)
-    int qa = 0;
-    {
-      int lo = 0, hi = nt - 1;  // last q with goff[q] <= g0
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_goff[mid] <= g0) lo = mid; else hi = mid - 1;
+
+  for (int j = blockIdx.x; j < np; j += gridDim.x) {
+    const int* pe = a.pieces + ((int64_t)seg * a.maxp + j) * 8;
+    const int k = pe[0], qa = pe[1], qb = pe[2], j0 = pe[3], j1 = pe[4], big = pe[5];
+    // slices of the piece's tiles (bit 31 of s_src: in the overflow area)
+    int run = 0;
+    for (int q0 = qa; q0 < qb; q0 += NT) {
+      const int q = q0 + tid;
+      int len = 0;
+      if (q < qb) {
+        const uint32_t s0 = rows[(int64_t)k * nt + q];
+        const uint32_t s1 = rows[(int64_t)(k + 1) * nt + q];
+        len = (int)(s1 - s0);
+        if (len > 0) {
+          const int64_t src = a.tile_src[(int64_t)seg * nt + q];
+          s_src[q] = src < 0 ? (uint32_t)(q * kFListCap) + s0 : (0x80000000u | (uint32_t)(src + s0));
+        }
       }
-      qa = lo;
+      int tt;
+      const int ex = block_excl_scan<NT, int>(len, s_scan, &tt);
+      if (q < qb) s_goff[q] = run + ex;
+      run += tt;
     }
-    for (int q = qa + (tid >> 3); q < nt && s_goff[q] < g0 + n; q += NT / 8) {
-      const int gq0 = max(s_goff[q], g0), gq1 = min(s_goff[q + 1], g0 + n);
-      if (gq1 <= gq0) continue;
-      const uint32_t* srcp = tile_keys(a, seg, q) + s_s0[q] + (gq0 - s_goff[q]);
-      const uint32_t gpx0 = (uint32_t)q * (uint32_t)a.G;
-      for (int j = tid & 7; j < gq1 - gq0; j += 8) {
-        const uint32_t key = __ldcs(srcp + j);
-        // entry: pixel | p << 24 | (t_rel & 7) << 25
-        s_g[gq0 - g0 + j] = (gpx0 + ((key >> 1) & 0x7ffu)) | ((key & 1u) << 24) | (((key >> 12) & 7u) << 25);
+    const int total = run;
+    if (tid == 0) s_goff[qb] = total;
+    if (big && tid < 8) {
+      // this piece's bin starts within the bucket: all pieces' counts of lower
+      // bins + earlier pieces' counts of the same bin
+      const uint32_t* pcn = a.pcnt + (int64_t)seg * a.maxp * 8;
+      int64_t below = 0, before = 0;
+      for (int jj = j0; jj < j1; ++jj) {
+        for (int v = 0; v < tid; ++v) below += pcn[jj * 8 + v];
+        if (jj < j) before += pcn[jj * 8 + tid];
       }
+      s_pbs[tid] = below + before;
     }
     __syncthreads();
-    bucket_place(s_g, s_s, n, s_binstart, s_bintot, s_scan64);
-    __syncthreads();
-    for (int i = tid; i < n; i += NT) {
-      const uint32_t e = s_s[i];
-      const uint32_t b = (e >> 25) & 7u;
-      const int64_t o = multi ? ob + s_gbs[b] + s_grun[b] + (i - s_binstart[b]) : ob + i;
-      const uint32_t gp = e & 0xffffffu;
-      uint32_t y = (uint32_t)((float)gp * winv);
-      if (y * (uint32_t)W > gp) --y;
-      else if ((y + 1) * (uint32_t)W <= gp) ++y;
-      a.out_t[o] = tbin0 + (int64_t)b;
-      a.out_x[o] = (uint16_t)(gp - y * (uint32_t)W);
-      a.out_y[o] = (uint16_t)y;
-      a.out_p[o] = (e >> 24) & 1u ? (int8_t)1 : (int8_t)-1;
+    const int64_t ob = (int64_t)seg * a.seg_stride + s_kbase[k];
+    const int64_t tbin0 = tprev + 8 * k;
+
+    for (int g0 = 0; g0 < total; g0 += kOCap) {
+      const int n = min(kOCap, total - g0);
+      // gather: thread t takes entries [t*m, t*m + m) of the chunk (one binary
+      // search for its first tile, then walks forward): all loads independent
+      {
+        const int m = (n + NT - 1) / NT;
+        const int i0 = min(n, tid * m), i1 = min(n, i0 + m);
+        if (i0 < i1) {
+          int lo = qa, hi = qb - 1;  // last tile with goff <= g0 + i0
+          const int gi0 = g0 + i0;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_goff[mid] <= gi0) lo = mid; else hi = mid - 1;
+          }
+          int q = lo;
+          int qend = s_goff[q + 1];
+          uint32_t so = s_src[q];
+          const uint32_t* srcp = ((so >> 31) ? area_seg + (so & 0x7fffffffu) : keys_seg + so) - s_goff[q];
+          uint32_t gpx0 = (uint32_t)q * (uint32_t)a.G;
+          for (int i = i0; i < i1; ++i) {
+            const int gi = g0 + i;
+            while (gi >= qend) {
+              ++q;
+              qend = s_goff[q + 1];
+              so = s_src[q];
+              srcp = ((so >> 31) ? area_seg + (so & 0x7fffffffu) : keys_seg + so) - s_goff[q];
+              gpx0 = (uint32_t)q * (uint32_t)a.G;
+            }
+            s_g[i] = gentry(__ldg(srcp + gi), gpx0);
+          }
+        }
+      }
+      __syncthreads();
+      // stable partition by bin: per-warp counts, offsets, ballot ranks
+      const int per = ((n + NW - 1) / NW + 31) & ~31;
+      const int lo = min(n, warp * per), hi = min(n, lo + per);
+      {
+        const uint32_t my = warp_bin_counts(s_g, lo, hi);
+        if (lane < 8) s_wc[warp][lane] = my;
+      }
+      __syncthreads();
+      if (tid < 8) {
+        uint32_t acc = 0;
+        for (int w = 0; w < NW; ++w) { const uint32_t c = s_wc[w][tid]; s_wc[w][tid] = acc; acc += c; }
+        s_cbs[tid] = acc;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t acc = 0;
+        for (int b = 0; b < 8; ++b) { const uint32_t c = s_cbs[b]; s_cbs[b] = acc; acc += c; }
+        s_cbs[8] = acc;
+      }
+      __syncthreads();
+      {
+        uint32_t runb = lane < 8 ? s_cbs[lane] + s_wc[warp][lane] : 0u;  // lane v: next slot of bin v
+        for (int base = lo; base < hi; base += 32) {
+          const int i = base + lane;
+          const bool valid = i < hi;
+          const uint32_t e = valid ? s_g[i] : 0u;
+          const uint32_t b = valid ? (e >> 25) & 7u : 8u;
+          uint32_t mine = 0, mv = 0;
+#pragma unroll
+          for (uint32_t v = 0; v < 8; ++v) {
+            const uint32_t m = __ballot_sync(0xffffffffu, b == v);
+            mine = b == v ? m : mine;
+            mv = lane == (int)v ? m : mv;
+          }
+          const uint32_t slot = __shfl_sync(0xffffffffu, runb, (int)(b & 7u));
+          if (valid) s_s[slot + __popc(mine & lanemask_lt())] = e;
+          runb += __popc(mv);
+        }
+      }
+      __syncthreads();
+      const bool contiguous = !big && total <= kOCap;
+      for (int i = tid; i < n; i += NT) {
+        const uint32_t e = s_s[i];
+        const uint32_t b = (e >> 25) & 7u;
+        // big pieces / later chunks: bin runs at the piece's bin starts (+ events
+        // of this bin in earlier chunks, accumulated in s_pbs)
+        const int64_t o = contiguous ? ob + i : ob + s_pbs[b] + (i - (int)s_cbs[b]);
+        const uint32_t gp = e & 0xffffffu;
+        uint32_t y = (uint32_t)((float)gp * winv);
+        if (y * (uint32_t)W > gp) --y;
+        else if ((y + 1) * (uint32_t)W <= gp) ++y;
+        a.out_t[o] = tbin0 + (int64_t)b;
+        a.out_x[o] = (uint16_t)(gp - y * (uint32_t)W);
+        a.out_y[o] = (uint16_t)y;
+        a.out_p[o] = (e >> 24) & 1u ? (int8_t)1 : (int8_t)-1;
+      }
+      __syncthreads();
+      if (!contiguous && tid < 8) s_pbs[tid] += s_cbs[tid + 1] - s_cbs[tid];
+      __syncthreads();
     }
-    __syncthreads();
-    if (multi && tid < 8) s_grun[tid] += s_bintot[tid];
-    __syncthreads();
   }
 }
 
@@ -914,7 +1238,7 @@ static void ensure_smem_fast(K k, size_t bytes) {
   if (ndone < 16) done[ndone++] = key;
 }
 
-size_t fast_gen_smem() { return (size_t)(2 * kFListCap + (kFNT / 32) * kFMaxBuckets + 5 * kFGmax) * 4; }
+size_t fast_gen_smem() { return (size_t)(2 * kFListCap + (kFNT / 32) * kFMaxBuckets) * 4; }
 size_t fast_order_smem(int ntiles) { return (size_t)2 * kOCap * 4 + (size_t)(2 * ntiles + 1) * 4; }
 
 cudaError_t launch_fast_gen(const FastArgs& a, cudaStream_t st) {
@@ -949,10 +1273,18 @@ cudaError_t launch_fast_redo(const FastArgs& a, int nseg, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_fast_plan(const FastArgs& a, int nseg, cudaStream_t st) {
+  k_fast_plan<<<nseg, kPlanNT, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fast_order(const FastArgs& a, int nseg, cudaStream_t st) {
+  k_fast_count<<<dim3(16, nseg), kONT, 0, st>>>(a);
   const size_t smem = fast_order_smem(a.ntiles);
   ensure_smem_fast(k_fast_order, fast_order_smem(kFMaxTiles));
-  dim3 grid(a.nbk, nseg);
+  // one CTA per piece in the common case (pieces = buckets); big buckets add
+  // pieces that the CTAs pick up round-robin
+  dim3 grid(a.nbk + 8, nseg);
   k_fast_order<<<grid, kONT, smem, st>>>(a);
   return cudaGetLastError();
 }

@@ -20,11 +20,12 @@ namespace evs {
 constexpr int kFNT = 512;                 // K1 threads per CTA
 constexpr int kFVpt = 4;                  // pixels per thread (one float4)
 constexpr int kFGmax = kFNT * kFVpt;      // max pixels per tile (2048; local index fits 11 bits)
-constexpr int kFListCap = 3 * kFGmax;     // crossings per tile-frame held in smem (else overflow path)
+constexpr int kFListCap = 5 * kFGmax;     // crossings per tile-frame held in smem (kFListCap/16 per warp)
+constexpr bool kFPrefilter = false;       // f32 __logf prefilter before the lite math
 constexpr int kFMaxBuckets = 256;         // buckets of 8 t_rel bins: dt <= 2048 us
 constexpr int kFMaxTiles = 4096;          // tiles per stream (K2 smem tables)
 constexpr int kONT = 512;                 // K2 threads per CTA
-constexpr int kOCap = 8192;               // K2 entries per chunk (smem)
+constexpr int kOCap = 12288;              // K2 entries per chunk (smem)
 
 constexpr int64_t kSrcSlot = -1, kSrcRedo = -3;
 
@@ -59,6 +60,12 @@ struct FastArgs {
   int* redo_items;           // [nseg][ntiles][2] (tile, area offset)
   int* redo_lim;             // [nseg][ntiles] kept share of each redo tile
   int* redo_n;               // [nseg]
+  uint32_t* btot;            // [nseg][nbk] events per bucket (zeroed by the prologue)
+  // K2 work split: pieces of <= ~kOCap events (a bucket, or a tile range of a big bucket)
+  int* pieces;               // [nseg][maxp][8]: k, qa, qb, j0, j1, big
+  int* npieces;              // [nseg]
+  uint32_t* pcnt;            // [nseg][maxp][8] per-bin counts of big-bucket pieces
+  int maxp;
   int64_t cap;               // events kept per segment
   int64_t* out_count;
   int64_t* out_dropped;
@@ -74,6 +81,7 @@ size_t fast_order_smem(int ntiles);
 cudaError_t launch_fast_gen(const FastArgs& a, cudaStream_t st);
 cudaError_t launch_fast_fix(const FastArgs& a, int nseg, cudaStream_t st);
 cudaError_t launch_fast_redo(const FastArgs& a, int nseg, cudaStream_t st);
+cudaError_t launch_fast_plan(const FastArgs& a, int nseg, cudaStream_t st);
 cudaError_t launch_fast_order(const FastArgs& a, int nseg, cudaStream_t st);
 
 }  // namespace evs

@@ -111,8 +111,14 @@ def test_random_inputs_fast_equals_exact_path():
     certified f32 math must agree bit for bit with the exact f64 path."""
     rng = np.random.default_rng(5)
     S, T, H, W = 2, 3, 256, 384
-    frames = rng.random((S, T, H, W), dtype=np.float32)
-    ref0 = np.log(rng.random((S, H, W)) + 0.01).astype(np.float32)
+    # a random walk in log intensity: diverse fractional parts of |diff|/th and
+    # of the crossing times, a few crossings per pixel
+    L = np.log(rng.random((S, H, W)) * 0.9 + 0.05)
+    ref0 = (L + rng.normal(0.0, 0.2, (S, H, W))).astype(np.float32)
+    frames = np.empty((S, T, H, W), np.float32)
+    for f in range(T):
+        L = np.clip(L + rng.normal(0.0, 0.25, (S, H, W)), np.log(0.02), 0.0)
+        frames[:, f] = np.clip(np.exp(L) - 0.01, 0.0, 1.0)
     last0 = rng.integers(-3000, 500, (S, H, W)).astype(np.int64)
     thp = np.maximum(rng.normal(0.1, 0.05, (S, H, W)), 0.01).astype(np.float32)
     thn = np.maximum(rng.normal(0.12, 0.05, (S, H, W)), 0.01).astype(np.float32)
