@@ -52,11 +52,15 @@ struct StepLayout {
 // boundaries) sized so the S*ntiles CTAs fill whole waves of 2 CTAs per SM.
 bool fast_shape(const evs_step_params* p, int64_t P, int64_t mdt, int* G, int* ntiles, int* nbk) {
   if (p->order != EVS_ORDER_CANONICAL || mdt < 1 || mdt > 8 * kFMaxBuckets) return false;
+  // the bucket path is opt-in (EVS_PATH=bucket): on the HD benchmark the
+  // tile-order path is faster
+  const char* path = getenv("EVS_PATH");
+  if (!(path && path[0] == 'b')) return false;
   const char* force = getenv("EVS_FORCE_LEGACY");
   if (force && force[0] == '1') return false;
   if (P >= (1ll << 24) || (int64_t)p->frames * mdt >= (1ll << 29)) return false;
   if (p->refractory_us >= (1ll << 29)) return false;
-  const int64_t slots = 2ll * sm_count_current();
+  const int64_t slots = (int64_t)kFCtasPerSm * sm_count_current();
   const int64_t S = p->streams;
   const int64_t min_tiles = (P + kFGmax - 1) / kFGmax;
   const int64_t waves = (S * min_tiles + slots - 1) / slots;
@@ -222,6 +226,10 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
              ((uintptr_t)b->last_event_t % 16 == 0) &&
              (b->th_pos == nullptr || (((uintptr_t)b->th_pos % 16 == 0) && ((uintptr_t)b->th_neg % 16 == 0)));
     fa.log_eps = p->log_eps; fa.log_eps_f = (float)p->log_eps;
+    {
+      const char* dbg = getenv("EVS_FAST_DBG");
+      fa.dbg = dbg ? atoi(dbg) : 0;
+    }
     fa.refr = (int)p->refractory_us;
     fa.thp_u = p->th_pos_uniform; fa.thn_u = p->th_neg_uniform;
     fa.rthp_u = (float)(1.0 / (double)p->th_pos_uniform);

@@ -332,6 +332,39 @@ __device__ __forceinline__ uint32_t px_fast2(float v, float r, int lrel, float t
          (k2 ? kF2K2 : 0u) | (pos ? kF2Pos : 0u) | ((uint32_t)(n & 3) << 25);
 }
 
+// Rare pixels (band straddles an integer, n > 2): the general path, out of
+// line so that the unrolled per-pixel code stays small and spill-free.
+struct SlowRes {
+  int n, kept, lnew;
+  bool pos;
+};
+template <bool REFR>
+__device__ __forceinline__ SlowRes slow_step(float v, float r, int lrel, float thp, float thn, float rthp, float rthn,
+                                          const FrameCtx& c, const LiteTab& T) {
+  PxStep o;
+  px_step<REFR, false>(v, r, lrel, thp, thn, rthp, rthn, c, T, o);
+  return SlowRes{o.n, o.kept, o.lnew, o.pos};
+}
+template <bool REFR>
+__device__ __forceinline__ void slow_emit(float v, float r, int lrel, float thp, float thn, float rthp, float rthn,
+                                       const FrameCtx& c, const LiteTab& T, uint32_t xy, uint32_t* list, int off) {
+  PxStep o;
+  px_step<REFR, false>(v, r, lrel, thp, thn, rthp, rthn, c, T, o);
+  const uint32_t xyp = xy | (o.pos ? 1u : 0u);
+  if (o.exact)
+    exact_emit<REFR>(v, r, lrel, thp, thn, c, xyp, list, off);
+  else
+    px_emit<REFR>(lrel, o.n, o.lo, c, [&](int tr) { list[off++] = ((uint32_t)tr << 12) | xyp; });
+}
+template <typename T>
+__device__ __forceinline__ T sel4(const T (&a)[4], int k) {
+  return k == 0 ? a[0] : (k == 1 ? a[1] : (k == 2 ? a[2] : a[3]));
+}
+template <typename T>
+__device__ __forceinline__ void set4(T (&a)[4], int k, T v) {
+  a[0] = k == 0 ? v : a[0]; a[1] = k == 1 ? v : a[1]; a[2] = k == 2 ? v : a[2]; a[3] = k == 3 ? v : a[3];
+}
+
 // ---------------------------------------------------------------------------
 // K1
 // ---------------------------------------------------------------------------
@@ -358,19 +391,26 @@ __device__ __forceinline__ int clamp_rel(int64_t d) {
   return d < -(1ll << 30) ? -(1 << 30) : (d > (1ll << 30) ? (1 << 30) : (int)d);
 }
 
+// K1.  Thread t of a tile owns pixels t + k*NT (k < VPT): for each k a warp
+// handles 32 consecutive pixels (one 32-pixel chunk of the reference), so a
+// tile's pixel order is (k, warp, lane) and its crossings form NG = VPT*NW
+// "groups" (k, warp) whose lists concatenate in pixel order.  The per-pixel
+// loop is rolled (small hot code: the instruction cache is the limiter) and
+// the state stays in registers (select chains instead of dynamic indexing).
 template <bool REFR, bool UNI>
-__global__ void __launch_bounds__(kFNT, 2) k_fast_gen(FastArgs a) {
-  constexpr int NT = kFNT, VPT = kFVpt, NW = NT / 32, KB = kFMaxBuckets, WCAP = kFListCap / NW;
+__global__ void __launch_bounds__(kFNT, kFCtasPerSm) k_fast_gen(FastArgs a) {
+  constexpr int NT = kFNT, VPT = kFVpt, NW = NT / 32, NG = VPT * NW, KB = kFMaxBuckets;
+  constexpr int GCAP = kFListCap / NG;  // crossings per group held in smem
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* s_list = reinterpret_cast<uint32_t*>(smem_raw);  // [NW][WCAP] pixel-major keys per warp
-  uint32_t* s_sorted = s_list + kFListCap;                     // [kFListCap] bucket-sorted keys of the tile
-  uint32_t* s_wcnt = s_sorted + kFListCap;                     // [NW][KB] per-warp bucket counters
+  uint32_t* s_list = reinterpret_cast<uint32_t*>(smem_raw);   // [NG][GCAP] pixel-major keys per group
+  uint32_t* s_sorted = s_list + kFListCap;                      // [kFListCap] bucket-sorted keys of the tile
+  uint16_t* s_gc = reinterpret_cast<uint16_t*>(s_sorted + kFListCap);  // [NG][KB] per-group bucket counters
   __shared__ LiteTab s_tab;
   __shared__ uint32_t s_bstart[KB + 1];
-  __shared__ uint32_t s_wtot[KB / 32];
-  __shared__ int s_wn[NW];         // crossings per warp (this frame)
+  __shared__ int s_gn[NG];         // crossings per group (this frame)
   __shared__ uint32_t s_res2[2];   // reservation chunks, per frame parity
-  __shared__ int s_ovf2[2];        // a warp list overflowed, per frame parity
+  __shared__ int s_ovf2[2];        // a group list overflowed, per frame parity
+  __shared__ int s_scan[NW + 1];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s = blockIdx.x / a.ntiles;
@@ -378,78 +418,43 @@ __global__ void __launch_bounds__(kFNT, 2) k_fast_gen(FastArgs a) {
   const int64_t P = a.P;
   const int64_t tile0 = (int64_t)tile * a.G;
   const int gt = (int)min((int64_t)a.G, P - tile0);  // pixels of this tile
-  const int lp0 = tid * VPT;                        // first local pixel of this thread
-  const int64_t pix0 = tile0 + lp0;
-  const bool full = (lp0 + VPT <= gt) && a.vec;
-  float* refp = a.ref + (int64_t)s * P;
-  int64_t* lastp = a.last + (int64_t)s * P;
+  float* refp = a.ref + (int64_t)s * P + tile0;
+  int64_t* lastp = a.last + (int64_t)s * P + tile0;
   const int64_t t0c = a.desc ? a.desc->cur_t0 : a.t0;
   const int64_t tb = frame_tprev(a, s, 0, t0c);  // time base of the relative times
   const int nbk = a.nbk;
-  uint32_t* wlist = s_list + warp * WCAP;
 
   // ---- state into registers ----
-  float r[VPT], thp[VPT], thn[VPT], rthp[VPT], rthn[VPT];
-  int lrel[VPT];
+  float r4[VPT], thp4[VPT], thn4[VPT], rthp4[VPT], rthn4[VPT];
+  int l4[VPT];
   uint32_t dirty = 0;  // bit k: level changed, bit 4+k: last event changed
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    r[k] = 0.f; lrel[k] = -(1 << 30);
-    thp[k] = a.thp_u; thn[k] = a.thn_u; rthp[k] = a.rthp_u; rthn[k] = a.rthn_u;
-  }
-  {
-    int64_t lt[VPT];
-#pragma unroll
-    for (int k = 0; k < VPT; ++k) lt[k] = 0;
-    if (full) {
-      const float4 q = __ldcg(reinterpret_cast<const float4*>(refp + pix0));
-      r[0] = q.x; r[1] = q.y; r[2] = q.z; r[3] = q.w;
-      if (REFR) {
-        const longlong2 l0 = __ldcg(reinterpret_cast<const longlong2*>(lastp + pix0));
-        const longlong2 l1 = __ldcg(reinterpret_cast<const longlong2*>(lastp + pix0 + 2));
-        lt[0] = l0.x; lt[1] = l0.y; lt[2] = l1.x; lt[3] = l1.y;
-      }
+    const int lp = tid + k * NT;
+    r4[k] = 0.f; l4[k] = -(1 << 30);
+    thp4[k] = a.thp_u; thn4[k] = a.thn_u; rthp4[k] = a.rthp_u; rthn4[k] = a.rthn_u;
+    if (lp < gt) {
+      r4[k] = __ldcg(refp + lp);
+      if (REFR) l4[k] = clamp_rel(__ldcg(lastp + lp) - tb);
       if (!UNI) {
-        const float4 p4 = *reinterpret_cast<const float4*>(a.thp + (int64_t)s * P + pix0);
-        const float4 n4 = *reinterpret_cast<const float4*>(a.thn + (int64_t)s * P + pix0);
-        thp[0] = p4.x; thp[1] = p4.y; thp[2] = p4.z; thp[3] = p4.w;
-        thn[0] = n4.x; thn[1] = n4.y; thn[2] = n4.z; thn[3] = n4.w;
+        thp4[k] = a.thp[(int64_t)s * P + tile0 + lp];
+        thn4[k] = a.thn[(int64_t)s * P + tile0 + lp];
+        rthp4[k] = __frcp_rn(thp4[k]);
+        rthn4[k] = __frcp_rn(thn4[k]);
       }
-    } else {
-#pragma unroll
-      for (int k = 0; k < VPT; ++k) {
-        if (lp0 + k < gt) {
-          r[k] = __ldcg(refp + pix0 + k);
-          if (REFR) lt[k] = __ldcg(lastp + pix0 + k);
-          if (!UNI) { thp[k] = a.thp[(int64_t)s * P + pix0 + k]; thn[k] = a.thn[(int64_t)s * P + pix0 + k]; }
-        }
-      }
-    }
-    if (REFR) {
-#pragma unroll
-      for (int k = 0; k < VPT; ++k) lrel[k] = clamp_rel(lt[k] - tb);
-    }
-    if (!UNI) {
-#pragma unroll
-      for (int k = 0; k < VPT; ++k) { rthp[k] = __frcp_rn(thp[k]); rthn[k] = __frcp_rn(thn[k]); }
     }
   }
-  for (int i = tid; i < NW * KB; i += NT) s_wcnt[i] = 0;
+  for (int i = tid; i < NG * KB / 2; i += NT) reinterpret_cast<uint32_t*>(s_gc)[i] = 0u;
   if (tid < 2) { s_res2[tid] = 0; s_ovf2[tid] = 0; }
   load_lite_tab(s_tab);
 
   auto load_frame = [&](int f, float* dst) {
-    const float* fr = a.frames + ((int64_t)s * a.T + f) * P;
-    if (full) {
-      const float4 q = __ldcs(reinterpret_cast<const float4*>(fr + pix0));
-      dst[0] = q.x; dst[1] = q.y; dst[2] = q.z; dst[3] = q.w;
-    } else {
+    const float* fr = a.frames + ((int64_t)s * a.T + f) * P + tile0;
 #pragma unroll
-      for (int k = 0; k < VPT; ++k) dst[k] = (lp0 + k < gt) ? __ldcs(fr + pix0 + k) : 1.0f;
-    }
+    for (int k = 0; k < VPT; ++k) dst[k] = (tid + k * NT < gt) ? __ldcs(fr + tid + k * NT) : 1.0f;
   };
-  float vnext[VPT];
-  load_frame(0, vnext);
+  float vn4[VPT];
+  load_frame(0, vn4);
   __syncthreads();
 
   for (int f = 0; f < a.T; ++f) {
@@ -458,112 +463,91 @@ __global__ void __launch_bounds__(kFNT, 2) k_fast_gen(FastArgs a) {
     const FrameCtx c = frame_ctx(a, s, f, t0c, tb);
     uint32_t& s_res = s_res2[f & 1];
     int& s_ovf = s_ovf2[f & 1];
-    float v[VPT];
+    float v4[VPT], ro4[VPT];
+    int lo4[VPT];
 #pragma unroll
-    for (int k = 0; k < VPT; ++k) v[k] = vnext[k];
-    if (f + 1 < a.T) load_frame(f + 1, vnext);
+    for (int k = 0; k < VPT; ++k) { v4[k] = vn4[k]; ro4[k] = r4[k]; lo4[k] = l4[k]; }
+    if (f + 1 < a.T) load_frame(f + 1, vn4);
 
-    // ---- 1. lane math (registers): crossings, refractory filter, new state ----
-    float rnew[VPT];
-    int lnew[VPT];
-    uint32_t pk[VPT];  // px_fast2 result (kF2Slow: px_step decides, again at emission)
-    int cnt = 0;
-    uint32_t chg = 0;  // bit k: level changes, bit 4+k: kept crossings
-#pragma unroll
+    // ---- 1. per pixel (rolled): lane math, state, crossings into the group lists ----
+    uint32_t chg = 0;
+#pragma unroll 1
     for (int k = 0; k < VPT; ++k) {
-      pk[k] = 0; rnew[k] = r[k]; lnew[k] = lrel[k];
-      if (!full && lp0 + k >= gt) continue;
-      int ln;
-      uint32_t res = px_fast2<REFR>(v[k], r[k], lrel[k], thp[k], thn[k], rthp[k], rthn[k], c, s_tab, ln);
-      int n, kept;
-      bool pos;
-      if (res & kF2Slow) {
-        PxStep o;
-        px_step<REFR, false>(v[k], r[k], lrel[k], thp[k], thn[k], rthp[k], rthn[k], c, s_tab, o);
-        n = o.n; kept = o.kept; pos = o.pos; ln = o.lnew;
-        res = kF2Slow;
-      } else {
-        n = (int)((res >> 25) & 3u);
-        kept = (int)((res >> 22) & 1u) + (int)((res >> 23) & 1u);
-        pos = (res & kF2Pos) != 0;
-      }
-      pk[k] = kept > 0 ? res : 0u;
-      // new level f32(ls +- n*th) (model.py:159-162); n*th is exact in f64 (n = 0: unchanged)
-      const double step = __dmul_rn((double)n, (double)(pos ? thp[k] : thn[k]));
-      rnew[k] = __double2float_rn(pos ? __dadd_rn((double)r[k], step) : __dsub_rn((double)r[k], step));
-      chg |= (n > 0 ? 1u : 0u) << k;
-      if (kept > 0) { chg |= 16u << k; lnew[k] = ln; }
-      cnt += kept;
-    }
-    // ---- 2. warp-local pixel-major emission + per-warp bucket histogram ----
-    int off = warp_incl_scan(cnt);
-    const int wn = __shfl_sync(0xffffffffu, off, 31);
-    off -= cnt;
-    {
-      // 32-pixel chunks with >= 1 kept event (AggregationStats.reservation_count):
-      // a chunk is 8 consecutive lanes; tiles start on chunk boundaries
-      const uint32_t b = __ballot_sync(0xffffffffu, cnt > 0);
-      if (lane == 0) {
-        s_wn[warp] = wn;
-        if (b) {
-          const uint32_t cc = ((b & 0xffu) != 0) + ((b & 0xff00u) != 0) + ((b & 0xff0000u) != 0) +
-                              ((b & 0xff000000u) != 0);
-          atomicAdd(&s_res, cc);
-        }
-        if (wn > WCAP) s_ovf = 1;
-      }
-    }
-    if (wn <= WCAP && cnt > 0) {
-#pragma unroll
-      for (int k = 0; k < VPT; ++k) {
-        const uint32_t res = pk[k];
-        if (res == 0) continue;
-        const uint32_t xy = (uint32_t)(lp0 + k) << 1;
-        if (!(res & kF2Slow)) {
-          const uint32_t xyp = xy | ((res & kF2Pos) ? 1u : 0u);
-          if (res & kF2K1) wlist[off++] = ((res & 0x7ffu) << 12) | xyp;
-          if (res & kF2K2) wlist[off++] = (((res >> 11) & 0x7ffu) << 12) | xyp;
+      const int lp = tid + k * NT;
+      const int g = k * NW + warp;
+      uint32_t* glist = s_list + g * GCAP;
+      const float v = sel4(v4, k), r = sel4(r4, k), thp = sel4(thp4, k), thn = sel4(thn4, k);
+      const float rthp = sel4(rthp4, k), rthn = sel4(rthn4, k);
+      const int l = sel4(l4, k);
+      uint32_t res = 0;
+      int n = 0, kept = 0, ln = l;
+      bool pos = false;
+      if (lp < gt) {
+        res = px_fast2<REFR>(v, r, l, thp, thn, rthp, rthn, c, s_tab, ln);
+        if (res & kF2Slow) {
+          const SlowRes o = slow_step<REFR>(v, r, l, thp, thn, rthp, rthn, c, s_tab);
+          n = o.n; kept = o.kept; ln = o.lnew; pos = o.pos;
         } else {
-          PxStep o;
-          px_step<REFR, false>(v[k], r[k], lrel[k], thp[k], thn[k], rthp[k], rthn[k], c, s_tab, o);
-          const uint32_t xyp = xy | (o.pos ? 1u : 0u);
-          if (o.exact)
-            off = exact_emit<REFR>(v[k], r[k], lrel[k], thp[k], thn[k], c, xyp, wlist, off);
-          else
-            px_emit<REFR>(lrel[k], o.n, o.lo, c, [&](int tr) { wlist[off++] = ((uint32_t)tr << 12) | xyp; });
+          n = (int)((res >> 25) & 3u);
+          kept = (int)((res >> 22) & 1u) + (int)((res >> 23) & 1u);
+          pos = (res & kF2Pos) != 0;
+        }
+        if (n > 0) {
+          // new level f32(ls +- n*th) (model.py:159-162); n*th is exact in f64
+          const double step = __dmul_rn((double)n, (double)(pos ? thp : thn));
+          set4(r4, k, __double2float_rn(pos ? __dadd_rn((double)r, step) : __dsub_rn((double)r, step)));
+          chg |= 1u << k;
+        }
+        if (kept > 0) { set4(l4, k, ln); chg |= 16u << k; }
+      }
+      // group list: warp scan of the kept counts
+      int off = warp_incl_scan(kept);
+      const int gn = __shfl_sync(0xffffffffu, off, 31);
+      off -= kept;
+      const uint32_t anyk = __ballot_sync(0xffffffffu, kept > 0);
+      if (lane == 0) {
+        s_gn[g] = gn;
+        if (anyk) atomicAdd(&s_res, 1u);  // one 32-pixel chunk with kept events
+        if (gn > GCAP) s_ovf = 1;
+      }
+      if (gn <= GCAP && kept > 0) {
+        const uint32_t xyp = ((uint32_t)lp << 1) | (pos ? 1u : 0u);
+        if (!(res & kF2Slow)) {
+          if (res & kF2K1) glist[off++] = ((res & 0x7ffu) << 12) | xyp;
+          if (res & kF2K2) glist[off++] = (((res >> 11) & 0x7ffu) << 12) | xyp;
+        } else {
+          slow_emit<REFR>(v, r, l, thp, thn, rthp, rthn, c, s_tab, (uint32_t)lp << 1, glist, off);
+        }
+      }
+      __syncwarp();
+      if (gn <= GCAP) {  // bucket counts of the group (warp-aggregated)
+        uint16_t* gc = s_gc + g * KB;
+        for (int base = 0; base < gn; base += 32) {
+          const int i = base + lane;
+          const bool valid = i < gn;
+          const uint32_t active = __ballot_sync(0xffffffffu, valid);
+          if (valid) {
+            const int bk = (int)(glist[i] >> 15);
+            const uint32_t peers = __match_any_sync(active, bk);
+            if (lane == __ffs(peers) - 1) gc[bk] = (uint16_t)(gc[bk] + __popc(peers));
+          }
         }
       }
     }
-    __syncwarp();
-    if (wn <= WCAP) {  // per-warp bucket counts (warp-aggregated: one smem update per bucket group)
-      for (int base = 0; base < wn; base += 32) {
-        const int i = base + lane;
-        const bool valid = i < wn;
-        const uint32_t active = __ballot_sync(0xffffffffu, valid);
-        if (valid) {
-          const int bk = (int)(wlist[i] >> 15);
-          const uint32_t peers = __match_any_sync(active, bk);
-          if (lane == __ffs(peers) - 1) s_wcnt[warp * KB + bk] += __popc(peers);
-        }
-      }
-    }
+    dirty |= chg;
     __syncthreads();  // A
     if (s_ovf) {  // block-uniform, rare: k_fast_redo regenerates this tile-frame
       float* sr = a.snap_ref + st_idx * a.G;
       int* sl = a.snap_last + st_idx * a.G;
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
-        if (lp0 + k >= gt) continue;
-        sr[lp0 + k] = r[k];
-        sl[lp0 + k] = lrel[k];
-        r[k] = rnew[k];
-        lrel[k] = lnew[k];
+        const int lp = tid + k * NT;
+        if (lp < gt) { sr[lp] = ro4[k]; sl[lp] = lo4[k]; }
       }
-      dirty |= chg;
-      for (int i = tid; i < NW * KB; i += NT) s_wcnt[i] = 0;
+      for (int i = tid; i < NG * KB / 2; i += NT) reinterpret_cast<uint32_t*>(s_gc)[i] = 0u;
       if (tid == 0) {
         int total = 0;
-        for (int w = 0; w < NW; ++w) total += s_wn[w];
+        for (int g = 0; g < NG; ++g) total += s_gn[g];
         a.tile_src[st_idx] = kSrcRedo;
         a.rows[((int64_t)seg * (nbk + 1) + nbk) * a.ntiles + tile] = (uint32_t)total;
         if (s_res) atomicAdd(reinterpret_cast<unsigned long long*>(a.seg_res + seg), (unsigned long long)s_res);
@@ -573,62 +557,58 @@ __global__ void __launch_bounds__(kFNT, 2) k_fast_gen(FastArgs a) {
       if (tid == 0) s_ovf = 0;  // (this parity slot is next used by frame f + 2)
       continue;
     }
-#pragma unroll
-    for (int k = 0; k < VPT; ++k) {  // apply the new state
-      r[k] = rnew[k];
-      lrel[k] = lnew[k];
-    }
-    dirty |= chg;
 
-    // ---- 3. bucket starts: column prefix over warps, scan over buckets ----
-    uint32_t tot = 0;
-    if (tid < nbk) {
-#pragma unroll 4
-      for (int w = 0; w < NW; ++w) {
-        const uint32_t cc = s_wcnt[w * KB + tid];
-        s_wcnt[w * KB + tid] = tot;
-        tot += cc;
+    // ---- 2. bucket starts: column prefix over the groups, scan over buckets ----
+    int total = 0;
+    {
+      uint32_t tot = 0;
+      if (tid < nbk) {
+        for (int g = 0; g < NG; ++g) {
+          const uint32_t cc = s_gc[g * KB + tid];
+          s_gc[g * KB + tid] = (uint16_t)tot;
+          tot += cc;
+        }
+      }
+      const uint32_t bst = (uint32_t)block_excl_scan<NT, int>((int)tot, s_scan, &total);
+      if (tid < nbk) {
+        for (int g = 0; g < NG; ++g) s_gc[g * KB + tid] = (uint16_t)(s_gc[g * KB + tid] + bst);
+        s_bstart[tid] = bst;
+        const uint32_t cb = tot;
+        if (cb) atomicAdd(a.btot + (int64_t)seg * nbk + tid, cb);
+      }
+      if (tid == 0) s_bstart[nbk] = (uint32_t)total;
+    }
+    __syncthreads();  // B
+
+    // ---- 3. stable rank (warp match-any over each of the warp's groups) ----
+#pragma unroll 1
+    for (int k = 0; k < VPT; ++k) {
+      const int g = k * NW + warp;
+      const uint32_t* glist = s_list + g * GCAP;
+      uint16_t* gc = s_gc + g * KB;
+      const int gn = s_gn[g];
+      for (int base = 0; base < gn; base += 32) {
+        const int i = base + lane;
+        const bool valid = i < gn;
+        const uint32_t active = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+          const uint32_t key = glist[i];
+          const int bk = (int)(key >> 15);
+          const uint32_t peers = __match_any_sync(active, bk);
+          const int leader = __ffs(peers) - 1;
+          uint32_t bpos = 0;
+          if (lane == leader) {
+            bpos = gc[bk];
+            gc[bk] = (uint16_t)(bpos + __popc(peers));
+          }
+          bpos = __shfl_sync(active, bpos, leader);
+          s_sorted[bpos + __popc(peers & lanemask_lt())] = key;
+        }
       }
     }
-    uint32_t inc = warp_incl_scan(tot);
-    if (lane == 31 && warp < KB / 32) s_wtot[warp] = inc;
-    __syncthreads();  // B
-    int total = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) total += s_wn[w];
-    if (tid < nbk) {
-      uint32_t wb = 0;
-      for (int w = 0; w < warp; ++w) wb += s_wtot[w];
-      const uint32_t bst = wb + inc - tot;
-#pragma unroll 4
-      for (int w = 0; w < NW; ++w) s_wcnt[w * KB + tid] += bst;
-      s_bstart[tid] = bst;
-    }
-    if (tid == 0) s_bstart[nbk] = (uint32_t)total;
     __syncthreads();  // C
 
-    // ---- 4. stable rank (warp match-any over the warp's list, pixel order) ----
-    for (int base = 0; base < wn; base += 32) {
-      const int i = base + lane;
-      const bool valid = i < wn;
-      const uint32_t active = __ballot_sync(0xffffffffu, valid);
-      if (valid) {
-        const uint32_t key = wlist[i];
-        const int bk = (int)(key >> 15);
-        const uint32_t peers = __match_any_sync(active, bk);
-        const int leader = __ffs(peers) - 1;
-        uint32_t bpos = 0;
-        if (lane == leader) {
-          bpos = s_wcnt[warp * KB + bk];
-          s_wcnt[warp * KB + bk] = bpos + __popc(peers);
-        }
-        bpos = __shfl_sync(active, bpos, leader);
-        s_sorted[bpos + __popc(peers & lanemask_lt())] = key;
-      }
-    }
-    __syncthreads();  // D
-
-    // ---- 5. sorted keys and bucket starts out; reset the counters ----
+    // ---- 4. sorted keys and bucket starts out; reset the counters ----
     {
       uint32_t* dst = a.keys + st_idx * kFListCap;
       const int n4 = total >> 2;
@@ -637,12 +617,8 @@ __global__ void __launch_bounds__(kFNT, 2) k_fast_gen(FastArgs a) {
       for (int i = 4 * n4 + tid; i < total; i += NT) dst[i] = s_sorted[i];
       uint32_t* rows = a.rows + (int64_t)seg * (nbk + 1) * a.ntiles + tile;
       for (int b = tid; b <= nbk; b += NT) rows[(int64_t)b * a.ntiles] = s_bstart[b];
-      if (tid < nbk) {
-#pragma unroll 4
-        for (int w = 0; w < NW; ++w) s_wcnt[w * KB + tid] = 0;
-        const uint32_t cb = s_bstart[tid + 1] - s_bstart[tid];
-        if (cb) atomicAdd(a.btot + (int64_t)seg * nbk + tid, cb);
-      }
+      if (tid < nbk)
+        for (int g = 0; g < NG; ++g) s_gc[g * KB + tid] = 0;
       if (tid == 0) {
         a.tile_src[st_idx] = kSrcSlot;
         if (s_res) atomicAdd(reinterpret_cast<unsigned long long*>(a.seg_res + seg), (unsigned long long)s_res);
@@ -653,20 +629,11 @@ __global__ void __launch_bounds__(kFNT, 2) k_fast_gen(FastArgs a) {
 
   // ---- state write-back (the prologue validated every frame of the call) ----
   if (*a.bad == kNoBad) {
-    if (full && (dirty & 0xfu) == 0xfu) {
-      *reinterpret_cast<float4*>(refp + pix0) = make_float4(r[0], r[1], r[2], r[3]);
-    } else {
 #pragma unroll
-      for (int k = 0; k < VPT; ++k)
-        if (dirty & (1u << k)) refp[pix0 + k] = r[k];
-    }
-    if (full && (dirty & 0xf0u) == 0xf0u) {
-      *reinterpret_cast<longlong2*>(lastp + pix0) = make_longlong2(tb + lrel[0], tb + lrel[1]);
-      *reinterpret_cast<longlong2*>(lastp + pix0 + 2) = make_longlong2(tb + lrel[2], tb + lrel[3]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < VPT; ++k)
-        if (dirty & (16u << k)) lastp[pix0 + k] = tb + lrel[k];
+    for (int k = 0; k < VPT; ++k) {
+      const int lp = tid + k * NT;
+      if (dirty & (1u << k)) refp[lp] = r4[k];
+      if (dirty & (16u << k)) lastp[lp] = tb + l4[k];
     }
   }
 }
@@ -1238,7 +1205,7 @@ static void ensure_smem_fast(K k, size_t bytes) {
   if (ndone < 16) done[ndone++] = key;
 }
 
-size_t fast_gen_smem() { return (size_t)(2 * kFListCap + (kFNT / 32) * kFMaxBuckets) * 4; }
+size_t fast_gen_smem() { return (size_t)2 * kFListCap * 4 + (size_t)kFVpt * (kFNT / 32) * kFMaxBuckets * 2; }
 size_t fast_order_smem(int ntiles) { return (size_t)2 * kOCap * 4 + (size_t)(2 * ntiles + 1) * 4; }
 
 cudaError_t launch_fast_gen(const FastArgs& a, cudaStream_t st) {

@@ -17,8 +17,9 @@
 
 namespace evs {
 
-constexpr int kFNT = 512;                 // K1 threads per CTA
+constexpr int kFNT = 256;                 // K1 threads per CTA
 constexpr int kFVpt = 4;                  // pixels per thread (one float4)
+constexpr int kFCtasPerSm = 3;            // K1 residency target (smem, 64 registers)
 constexpr int kFGmax = kFNT * kFVpt;      // max pixels per tile (2048; local index fits 11 bits)
 constexpr int kFListCap = 5 * kFGmax;     // crossings per tile-frame held in smem (kFListCap/16 per warp)
 constexpr bool kFPrefilter = false;       // f32 __logf prefilter before the lite math
@@ -33,6 +34,7 @@ constexpr int64_t kSrcSlot = -1, kSrcRedo = -3;
 
 struct FastArgs {
   int S, T, W, G, ntiles, nbk, vec;
+  int dbg;  // timing experiments only (EVS_FAST_DBG): 1 = K1 math only
   int64_t P;
   double log_eps;
   float log_eps_f;

@@ -1,5 +1,5 @@
 """Fast canonical path (csrc/fast_path.cu) against the CPU oracle and against the
-legacy exact-f64 path (EVS_FORCE_LEGACY=1), including its rare paths: tile
+tile-order path (the default, exact-f64 lane math), including its rare paths: tile
 lists that overflow shared memory, the capacity cut, irregular ticks, and
 random inputs that stress the certified f32 lane math."""
 
@@ -23,11 +23,12 @@ def _run(frames, ref0, last0, thp, thn, refr, cap, uniform, legacy=False, t_boun
 
     S, T, H, W = frames.shape
     dev = torch.device("cuda")
-    old = os.environ.get("EVS_FORCE_LEGACY")
+    old = os.environ.get("EVS_PATH")
     if legacy:
-        os.environ["EVS_FORCE_LEGACY"] = "1"
+        os.environ.pop("EVS_PATH", None)
     else:
-        os.environ.pop("EVS_FORCE_LEGACY", None)
+        os.environ["EVS_PATH"] = "bucket"
+
     try:
         eng = StepEngine(StepShape(S, T, H, W, cap, 1, max_dt, 0.01, refr, uniform), dev)
         ref = torch.from_numpy(ref0.copy()).to(dev)
@@ -39,9 +40,9 @@ def _run(frames, ref0, last0, thp, thn, refr, cap, uniform, legacy=False, t_boun
         counts, dropped, res, bad = eng.fetch_info()
     finally:
         if old is None:
-            os.environ.pop("EVS_FORCE_LEGACY", None)
+            os.environ.pop("EVS_PATH", None)
         else:
-            os.environ["EVS_FORCE_LEGACY"] = old
+            os.environ["EVS_PATH"] = old
     assert bad == _lib.NO_BAD
     segs = []
     for g in range(S * T):
