@@ -11,7 +11,7 @@ from __future__ import annotations
 import numpy as np
 
 from .. import _lib
-from ..runtime import StepEngine, StepShape, upload_frame
+from ..runtime import PinnedPool, StepEngine, StepShape, d2h_rows, upload_frame
 from .types import (
     MIN_THRESHOLD,
     DeviceEventBatch,
@@ -139,14 +139,12 @@ def run_generate(state: PixelStateGrid, frame: IntensityFrame, t_prev: int, t_no
     if n == 0:
         b = EventBatch.empty(dropped_count=int(dropped[0]))
     else:
-        b = EventBatch(
-            t=eng.ev_t[0, :n].cpu().numpy().view(np.uint64),
-            x=eng.ev_x[0, :n].cpu().numpy().view(np.uint16),
-            y=eng.ev_y[0, :n].cpu().numpy().view(np.uint16),
-            polarity=eng.ev_p[0, :n].cpu().numpy(),
-            dropped_count=int(dropped[0]),
-            canonical=order == _lib.EVS_ORDER_CANONICAL,
-        )
+        # fresh pinned host arrays (torch's caching host allocator recycles the
+        # blocks once the caller drops the batch): one async copy each, one sync
+        pool = state._ctx.setdefault("d2h_pool", PinnedPool())
+        t, x, y, p = d2h_rows(pool, n, [eng.ev_t[0], eng.ev_x[0], eng.ev_y[0], eng.ev_p[0]])
+        b = EventBatch(t=t.view(np.uint64), x=x.view(np.uint16), y=y.view(np.uint16), polarity=p,
+                       dropped_count=int(dropped[0]), canonical=order == _lib.EVS_ORDER_CANONICAL)
     if stats is not None and getattr(stats, "collect_spans", False):
         stats.write_spans = _chunk_spans(b, state.width)
     return b

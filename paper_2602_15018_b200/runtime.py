@@ -187,21 +187,96 @@ class StepEngine:
         self.bad.fill_(_lib.NO_BAD)
 
 
+class PinnedPool:
+    """Reusable pinned host blocks for device->host result copies.
+
+    Results are handed out as numpy views into a block; a block is reused
+    only once no view of it is alive (the views keep the block's root array
+    referenced), so returned arrays stay valid for as long as the caller holds
+    them -- the same ownership the reference's freshly allocated arrays have.
+    """
+
+    def __init__(self, keep: int = 8):
+        self.roots = []  # (pinned uint8 tensor, its numpy root array)
+        self.keep = keep
+
+    def take(self, nbytes: int):
+        import sys
+
+        import torch
+
+        for i, (t, r) in enumerate(self.roots):
+            if r.nbytes >= nbytes and sys.getrefcount(r) <= 3:  # list tuple + r + the call
+                return t, r
+        size = 1 << 20
+        while size < nbytes:  # power-of-two blocks: varying batch sizes reuse them
+            size <<= 1
+        t = torch.empty(size, dtype=torch.uint8, pin_memory=True)
+        r = t.numpy()
+        self.roots.append((t, r))
+        if len(self.roots) > self.keep:  # forget the oldest idle block
+            for i, (_t, rr) in enumerate(self.roots[:-1]):
+                if sys.getrefcount(rr) <= 3:
+                    del self.roots[i]
+                    break
+        return t, r
+
+
+def d2h_rows(pool: PinnedPool, n: int, rows, stream=None):
+    """Copy the first n elements of each device tensor in `rows` into one pinned
+    block (async copies, one synchronize); returns numpy views into it."""
+    import torch
+
+    sizes = [n * r.element_size() for r in rows]
+    offs, o = [], 0
+    for sz in sizes:
+        offs.append(o)
+        o += (sz + 255) // 256 * 256
+    t, root = pool.take(o)
+    for r, off, sz in zip(rows, offs, sizes):
+        if n:
+            t[off:off + sz].view(r.dtype).copy_(r[:n], non_blocking=True)
+    (stream or torch.cuda.current_stream()).synchronize()
+    np_dt = {torch.int64: np.int64, torch.int16: np.int16, torch.int8: np.int8, torch.int32: np.int32,
+             torch.float32: np.float32, torch.uint8: np.uint8}
+    return [root[off:off + sz].view(np_dt[r.dtype]) for r, off, sz in zip(rows, offs, sizes)]
+
+
+def d2h_segments(pool: PinnedPool, counts, rows2d, stream=None):
+    """Device [nseg][cap] output pools -> host: the first counts[g] elements of
+    every segment, packed per row into one pinned block (async copies, one
+    synchronize).  Returns, per row, a list of per-segment numpy views."""
+    import torch
+
+    counts = [int(c) for c in counts]
+    total = sum(counts)
+    offs, o = [], 0
+    for r in rows2d:
+        offs.append(o)
+        o += (total * r.element_size() + 255) // 256 * 256
+    t, root = pool.take(max(o, 1))
+    np_dt = {torch.int64: np.int64, torch.int16: np.int16, torch.int8: np.int8}
+    out = []
+    for r, base in zip(rows2d, offs):
+        es = r.element_size()
+        views, e = [], 0
+        for g, n in enumerate(counts):
+            if n:
+                t[base + e * es:base + (e + n) * es].view(r.dtype).copy_(r[g, :n], non_blocking=True)
+            views.append(root[base + e * es:base + (e + n) * es].view(np_dt[r.dtype]))
+            e += n
+        out.append(views)
+    (stream or torch.cuda.current_stream()).synchronize()
+    return out
+
+
 def upload_frame(values, device, staging_cache: dict | None = None):
-    """Host numpy (H, W) float32 -> device tensor (via a cached pinned buffer)."""
+    """Host numpy (H, W) float32 -> device tensor.  A direct copy from the
+    caller's pageable array (the driver stages it) measured faster than an
+    extra memcpy into a pinned buffer; ``staging_cache`` is kept for callers."""
     import torch
 
     if type(values).__module__.startswith("torch"):
         return values.to(device=device, dtype=torch.float32).contiguous()
     arr = np.ascontiguousarray(values, np.float32)
-    if staging_cache is not None:
-        key = ("stage", arr.shape)
-        pin = staging_cache.get(key)
-        if pin is None:
-            pin = torch.empty(arr.shape, dtype=torch.float32, pin_memory=True)
-            staging_cache[key] = pin
-        pin.numpy()[...] = arr
-        out = torch.empty(arr.shape, dtype=torch.float32, device=device)
-        out.copy_(pin, non_blocking=True)
-        return out
     return torch.from_numpy(arr).to(device)

@@ -131,6 +131,37 @@ class EventSimulator:
         return DeviceEventBatch(e.ev_t[g, :n], e.ev_x[g, :n], e.ev_y[g, :n], e.ev_p[g, :n],
                                 dropped_count=int(e.info[1, g].item()), canonical=self.canonical)
 
+    def step_host(self, frames_host, validate: bool = True):
+        """Host-buffer counterpart of step(): frames_host is a float32 numpy array
+        [S, T, H, W] (or [S, H, W] when T == 1); returns the events of every
+        (stream, frame) as host EventBatch objects, list [S][T], canonical order.
+        The result arrays are views into reusable pinned blocks (valid while held)."""
+        import torch
+
+        from .events.types import EventBatch
+        from .runtime import PinnedPool, d2h_segments
+
+        fr = np.ascontiguousarray(frames_host, np.float32)
+        if fr.ndim == 3:
+            fr = fr[:, None]
+        dfr = torch.from_numpy(fr).to(self.device)
+        self.step(dfr, validate=validate)
+        res = self.result()
+        if not hasattr(self, "_pool"):
+            self._pool = PinnedPool()
+        e = self.engine
+        t, x, y, p = d2h_segments(self._pool, res.counts.ravel(), [e.ev_t, e.ev_x, e.ev_y, e.ev_p])
+        out = []
+        for s in range(self.S):
+            row = []
+            for f in range(self.T):
+                g = s * self.T + f
+                row.append(EventBatch(t=t[g].view(np.uint64), x=x[g].view(np.uint16), y=y[g].view(np.uint16),
+                                      polarity=p[g], dropped_count=int(res.dropped[s, f]),
+                                      canonical=self.canonical))
+            out.append(row)
+        return out
+
     # -- CUDA graph replay -------------------------------------------------------
     def capture(self, frame_windows) -> None:
         """Capture one graph stepping through `frame_windows` ([S, T, H, W] each) in order."""
