@@ -35,6 +35,7 @@
 #include "common.cuh"
 #include "fast_path.cuh"
 #include "log_table.h"
+#include "lane_lite.cuh"
 
 namespace evs {
 
@@ -100,32 +101,9 @@ __device__ __forceinline__ int exact_trel(int j, double thd, double ad, double d
 // ---------------------------------------------------------------------------
 // certified f32 lane math
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float rcp_approx(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
 // |df - diff_ref| <= kEpsD + 3*2^-24*|df| (see the header comment of
 // fast_path.cuh); diff_ref is the reference's f64 ln(v + eps) - ref.
 // (kEpsD = 8e-9 enters the bands below as the 1e-8 terms.)
-
-struct LiteOut {
-  float uf;    // t_rel(j) ~ j * uf
-  float erel;  // relative band of j * uf
-};
-
-// Table of the lite log (shared memory): c_i, 1/c_i, log(c_i) (hi part).
-struct LiteTab {
-  double c[128], invc[128], lh[128];
-};
-__device__ __forceinline__ void load_lite_tab(LiteTab& t) {
-  for (int i = threadIdx.x; i < 128; i += blockDim.x) {
-    t.c[i] = kLogTable[i][0];
-    t.invc[i] = kLogTable[i][1];
-    t.lh[i] = kLogTable[i][2];
-  }
-}
 
 // All roundings below are explicit (_rn intrinsics / fmaf) so that no FMA
 // contraction can differ between the passes that evaluate the same pixel
@@ -175,13 +153,6 @@ __device__ __forceinline__ int lite_trel(int j, const LiteOut& o, int dtm1) {
   const int hi = min((int)floorf(__fadd_rn(a, band)), dtm1);
   return lo == hi ? lo : -1;
 }
-
-// Per-frame constants of the lane math.
-struct FrameCtx {
-  double log_eps, dtd;
-  float log_eps_f, dtf;
-  int dtm1, tpr, refr;  // tpr: frame start relative to the call's time base
-};
 
 // One pixel, one frame (model.py:124-163): n (level steps), kept crossings
 // after the refractory filter, and the last kept time.
@@ -279,57 +250,6 @@ __device__ __forceinline__ void px_emit(int lold, int n, const LiteOut& lo, cons
     }
     sink(tr);
   }
-}
-
-// Straight-line lane math for the common case n <= 2 (no loops, no branches):
-// the same certified f32 evaluation as lite_count / lite_trel.  Returns
-//   bits 0-10 t_rel(1), 11-21 t_rel(2), 22 kept(1), 23 kept(2), 24 pos,
-//   25-26 n (0..2), 31 slow (band straddles an integer, n > 2, or x outside
-//   the table's range: px_step decides),
-// and the last kept time in lnew.  dt <= 2048 (11-bit t_rel).
-constexpr uint32_t kF2Slow = 0x80000000u, kF2K1 = 1u << 22, kF2K2 = 1u << 23, kF2Pos = 1u << 24;
-template <bool REFR>
-__device__ __forceinline__ uint32_t px_fast2(float v, float r, int lrel, float thp, float thn, float rthp,
-                                             float rthn, const FrameCtx& c, const LiteTab& T, int& lnew) {
-  const double x = __dadd_rn((double)v, c.log_eps);
-  const uint64_t ix = (uint64_t)__double_as_longlong(x);
-  const bool bad_x = ix < 0x0010000000000000ull || ix >= 0x7ff0000000000000ull;
-  const uint64_t tmp = ix - kLogOff;
-  const int i = (int)((tmp >> (52 - kLogTableBits)) & ((1u << kLogTableBits) - 1));
-  const int k = (int)((int64_t)tmp >> 52);
-  const double z = __longlong_as_double((long long)(ix - (tmp & 0xfff0000000000000ull)));
-  const double d = __dsub_rn(z, T.c[i]);
-  const float rf = __double2float_rn(__dmul_rn(d, T.invc[i]));
-  float pf = fmaf(rf, 0.2f, -0.25f);
-  pf = fmaf(pf, rf, 0.33333334f);
-  pf = fmaf(pf, rf, -0.5f);
-  pf = fmaf(pf, rf, 1.0f);
-  pf = __fmul_rn(pf, rf);
-  const double dd = __dsub_rn(fma((double)k, 0.6931471805599453, T.lh[i]), (double)r);
-  const float df = __fadd_rn(__double2float_rn(dd), pf);
-  const bool pos = df > 0.f;
-  const float ad = fabsf(df);
-  const float th = pos ? thp : thn;
-  const float rth = pos ? rthp : rthn;
-  const float q1 = fmaf(ad, rth, 1e-4f);
-  const float dn = fmaf(q1, 6e-7f, fmaf(1e-8f, rth, 1e-10f));
-  const float nlo = floorf(__fsub_rn(q1, dn)), nhi = floorf(__fadd_rn(q1, dn));
-  const int n = (int)nlo;
-  const float ra = rcp_approx(ad);
-  const float uf = __fmul_rn(__fmul_rn(th, c.dtf), ra);
-  const float erel = fmaf(1e-8f, ra, 1e-6f);
-  const float a1 = __fmul_rn(1.0f, uf), a2 = __fmul_rn(2.0f, uf);
-  const float b1 = fmaf(a1, erel, 1e-6f), b2 = fmaf(a2, erel, 1e-6f);
-  const int t1 = min((int)floorf(__fsub_rn(a1, b1)), c.dtm1), t1h = min((int)floorf(__fadd_rn(a1, b1)), c.dtm1);
-  const int t2 = min((int)floorf(__fsub_rn(a2, b2)), c.dtm1), t2h = min((int)floorf(__fadd_rn(a2, b2)), c.dtm1);
-  const bool slow = bad_x | (nlo != nhi) | (q1 > 1e6f) | (n > 2) | ((n >= 1) & (t1 != t1h)) |
-                    ((n >= 2) & (t2 != t2h));
-  const bool k1 = (n >= 1) && (!REFR || c.tpr + t1 - lrel >= c.refr);
-  const int l1 = k1 ? c.tpr + t1 : lrel;
-  const bool k2 = (n >= 2) && (!REFR || c.tpr + t2 - l1 >= c.refr);
-  lnew = k2 ? c.tpr + t2 : l1;
-  return (slow ? kF2Slow : 0u) | ((uint32_t)(t1 & 0x7ff)) | ((uint32_t)(t2 & 0x7ff) << 11) | (k1 ? kF2K1 : 0u) |
-         (k2 ? kF2K2 : 0u) | (pos ? kF2Pos : 0u) | ((uint32_t)(n & 3) << 25);
 }
 
 // Rare pixels (band straddles an integer, n > 2): the general path, out of
