@@ -4,7 +4,7 @@
 Workload (BASELINE.json configs[1]): HD 1280x720 camera, C=0.15, refractory
 100 us, 1000 us ticks, synthetic moving texture (events_bench.py:19-26),
 time-ordered (t, x, y, p) output per frame.  A "step" is one evs_step over T
-consecutive frames of the camera (default T=25; every frame still gets its
+consecutive frames of the camera (default T=50; every frame still gets its
 own canonical event segment); the same workload at one frame per launch (the
 reference's per-frame call granularity) is reported in "per_frame_launch".
 Frames cycle through a pre-generated ring of lcm(T, 50) frames (>= 184 MB >
@@ -391,6 +391,14 @@ def run_ours(args):
     fps = frames_total / (ms / 1e3)
     ev_s = world * E_last * K / (ms / 1e3)
     peak, peak_kind = measured_peak_hbm()
+    traffic = None
+    try:  # ncu dram bytes of one step of this workload (committed profile)
+        with open(os.path.join(ROOT, "profiles", "r1_step_traffic.json")) as fh:
+            tr = json.load(fh)
+        if int(tr["frames_per_step"]) == T:
+            traffic = int(tr["bytes_per_step"])
+    except Exception:
+        traffic = None
     E_frame = E_step / T
     B = algorithmic_bytes(P, A, E_step, REFR, st.uniform_thresholds is not None, T)
     # the hot-path unit is one evs_step (4 launches); its duration is the
@@ -420,7 +428,8 @@ def run_ours(args):
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "mevents_per_s": ev_s / 1e6, "events_per_frame": E_frame, "active_px_per_step": A,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "traffic_note": "dram read+write bytes per step from ncu (profiles/r1_step_traffic.json)",
                      "kernel": "evs_step (k_prologue + k_generate + k_tilescan + k_tile_order), "
                                "device time per step of the timed region",
                      "algorithmic_bytes_per_step": B,
@@ -445,7 +454,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--frames-per-step", type=int, default=25)
+    ap.add_argument("--frames-per-step", type=int, default=50)
     ap.add_argument("--compare-t1", type=int, default=1)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
