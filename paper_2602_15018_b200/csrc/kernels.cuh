@@ -13,7 +13,6 @@ constexpr int kKeyPixBits = 33;   // key = t_rel << 33 | y << 17 | x << 1 | (p >
 constexpr int kGenThreads = 256;
 constexpr int kGenVpt = 4;
 constexpr int kGenTile = kGenThreads * kGenVpt;  // pixels per K1 tile
-constexpr int kGenStage = 4 * kGenTile;          // staged keys per tile (smem)
 
 constexpr int kOrdThreads = 256;
 constexpr int kOrdIpt = 16;
@@ -128,36 +127,7 @@ struct TileOrderArgs {
 cudaError_t launch_tilescan(const TileScanArgs& a, cudaStream_t st);
 cudaError_t launch_tile_order(const TileOrderArgs& a, cudaStream_t st);
 
-constexpr int kGroupTiles = 4;      // legacy group size (generic path)
 constexpr int kMaxGroupTiles = 16;  // K1 tiles per histogram row / per K2 CTA (runtime gt <= this)
-
-struct ColScanArgs {
-  int nseg, ngroups, bits;
-  int64_t cap;
-  uint32_t* rows;             // in: counts, out: exclusive prefix over groups
-  uint32_t* tot;              // out [nseg][NB]
-  const int64_t* seg_total;
-  int64_t* out_count;
-  int64_t* out_dropped;
-  const int64_t* bad;
-};
-
-struct GroupOrderArgs {
-  int nseg, ngroups, bits, shift;
-  const uint64_t* keys_in;
-  int64_t seg_stride;
-  uint32_t* rows;             // exclusive group prefixes (zeroed after use)
-  const uint32_t* tot;        // [nseg][NB]
-  const int64_t* group_base;  // [nseg][ngroups]
-  const int64_t* seg_count;   // written events per segment
-  int final_soa;
-  uint64_t* keys_out;
-  int64_t* out_t;
-  uint16_t* out_x;
-  uint16_t* out_y;
-  int8_t* out_p;
-  const int64_t* seg_tbase;
-};
 
 struct PlanArgs {
   int nseg;
@@ -213,9 +183,7 @@ cudaError_t launch_generate(const GenArgs& a, int uniform_th, cudaStream_t st);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t st);
 cudaError_t launch_hist(const HistArgs& a, cudaStream_t st);
 cudaError_t launch_order(const OrderArgs& a, int sm_count, cudaStream_t st);
-cudaError_t launch_colscan(const ColScanArgs& a, cudaStream_t st);
 cudaError_t launch_selftest_log(const double* x, double* out_fast, double* out_ref, int64_t n,
                                 cudaStream_t st);
-cudaError_t launch_group_order(const GroupOrderArgs& a, cudaStream_t st);
 
 }  // namespace evs

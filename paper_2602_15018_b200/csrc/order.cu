@@ -390,203 +390,5 @@ cudaError_t launch_order(const OrderArgs& a, int sm_count, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------
-// column scan: per (segment, bin) exclusive prefix of the tile-group
-// histogram rows over groups (pixel order) + bin totals; counts/capacity.
-// ---------------------------------------------------------------------------
-// Block = 32 bins x 16 group-chunks: every thread issues its chunk's loads
-// at once (one L2 round trip), then chunk sums are scanned in smem.
-constexpr int kCsBins = 32, kCsChunks = 16;
-__global__ void __launch_bounds__(kCsBins * kCsChunks) k_colscan(ColScanArgs a) {
-  __shared__ uint32_t s_sum[kCsChunks][kCsBins];
-  const int NB = 1 << a.bits;
-  const int seg = blockIdx.y;
-  const int bl = threadIdx.x % kCsBins, ch = threadIdx.x / kCsBins;
-  const int d = blockIdx.x * kCsBins + bl;
-  const bool bad = *a.bad != kNoBad;
-  if (blockIdx.x == 0 && threadIdx.x == 0 && a.out_count) {
-    const int64_t total = bad ? 0 : a.seg_total[seg];
-    const int64_t w = total < a.cap ? total : a.cap;
-    a.out_count[seg] = w;
-    a.out_dropped[seg] = total - w;
-  }
-  const int CH = (a.ngroups + kCsChunks - 1) / kCsChunks;
-  const int g0 = ch * CH, g1 = min(a.ngroups, g0 + CH);
-  uint32_t* col = a.rows + (int64_t)seg * a.ngroups * NB + d;
-  constexpr int kMaxCh = 32;
-  uint32_t c[kMaxCh];
-  uint32_t sum = 0;
-  if (d < NB) {
-#pragma unroll
-    for (int u = 0; u < kMaxCh; ++u) c[u] = (g0 + u < g1) ? col[(int64_t)(g0 + u) * NB] : 0u;
-    // (groups beyond kMaxCh per chunk are handled by the tail loop below)
-#pragma unroll
-    for (int u = 0; u < kMaxCh; ++u) sum += c[u];
-    for (int g = g0 + kMaxCh; g < g1; ++g) sum += col[(int64_t)g * NB];
-  }
-  s_sum[ch][bl] = sum;
-  __syncthreads();
-  uint32_t acc = 0, tot = 0;
-  for (int k = 0; k < kCsChunks; ++k) {
-    const uint32_t v = s_sum[k][bl];
-    if (k < ch) acc += v;
-    tot += v;
-  }
-  if (d < NB) {
-#pragma unroll
-    for (int u = 0; u < kMaxCh; ++u)
-      if (g0 + u < g1) { col[(int64_t)(g0 + u) * NB] = acc; acc += c[u]; }
-    for (int g = g0 + kMaxCh; g < g1; ++g) {
-      const uint32_t v = col[(int64_t)g * NB];
-      col[(int64_t)g * NB] = acc;
-      acc += v;
-    }
-    if (ch == 0) a.tot[(int64_t)seg * NB + d] = bad ? 0u : tot;
-  }
-}
-
-cudaError_t launch_colscan(const ColScanArgs& a, cudaStream_t st) {
-  const int NB = 1 << a.bits;
-  dim3 grid((NB + kCsBins - 1) / kCsBins, a.nseg);
-  k_colscan<<<grid, kCsBins * kCsChunks, 0, st>>>(a);
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// K2 (group form): one CTA per (segment, tile group).  The group's keys are
-// already in pixel order; a stable counting pass by t_rel places them at
-// bin start + prefix of earlier groups (column scan) + running sub-tile
-// offset + warp match-any rank.  No inter-CTA waiting.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kOrdThreads) k_group_order(GroupOrderArgs a) {
-  constexpr int NT = kOrdThreads, IPT = kOrdIpt, M = kOrdTile, NW = NT / 32;
-  extern __shared__ __align__(16) unsigned char sm[];
-  const int NB = 1 << a.bits;
-  uint64_t* sorted = reinterpret_cast<uint64_t*>(sm);
-  uint16_t* wcnt = reinterpret_cast<uint16_t*>(sorted + M);  // [NW][NB]
-  uint32_t* lstart = reinterpret_cast<uint32_t*>(wcnt + NW * NB);
-  uint32_t* offr = lstart + NB;
-  uint32_t* stot = offr + NB;
-  __shared__ uint32_t s_scan[NW + 1];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int seg = blockIdx.y, g = blockIdx.x;
-  const uint64_t dmask = (uint64_t)(NB - 1);
-  const int per = (NB + NT - 1) / NT;
-
-  const int64_t n = a.seg_count[seg];
-  int64_t lo = a.group_base[(int64_t)seg * a.ngroups + g];
-  int64_t hi = (g + 1 < a.ngroups) ? a.group_base[(int64_t)seg * a.ngroups + g + 1] : n;
-  lo = lo < n ? lo : n;
-  hi = hi < n ? hi : n;
-  if (n == 0) lo = hi = 0;
-
-  // running global offset per bin: bin start (scan of totals) + earlier groups
-  uint32_t* row = a.rows + ((int64_t)seg * a.ngroups + g) * NB;
-  {
-    uint32_t sum = 0;
-    for (int j = 0; j < per; ++j) { const int d = tid * per + j; if (d < NB) sum += a.tot[(int64_t)seg * NB + d]; }
-    uint32_t tt;
-    uint32_t ex = block_excl_scan<NT, uint32_t>(sum, s_scan, &tt);
-    for (int j = 0; j < per; ++j) {
-      const int d = tid * per + j;
-      if (d < NB) {
-        offr[d] = ex + row[d];
-        row[d] = 0;  // rows are accumulated with atomics by the next step's K1
-        ex += a.tot[(int64_t)seg * NB + d];
-      }
-    }
-  }
-  __syncthreads();
-  const uint64_t* kin = a.keys_in + (int64_t)seg * a.seg_stride;
-  const int64_t ob = (int64_t)seg * a.seg_stride;
-  const int64_t tb0 = a.seg_tbase ? a.seg_tbase[seg] : 0;
-
-  for (int64_t base = lo; base < hi; base += M) {
-    const int cnt = (int)((hi - base) < M ? (hi - base) : M);
-    for (int d = lane; d < NB; d += 32) wcnt[warp * NB + d] = 0;
-    __syncwarp();
-    uint64_t key[IPT];
-    uint32_t rank[IPT];
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      const int idx = warp * 32 * IPT + k * 32 + lane;
-      key[k] = idx < cnt ? __ldcs(kin + base + idx) : 0ull;
-    }
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      const int idx = warp * 32 * IPT + k * 32 + lane;
-      const bool valid = idx < cnt;
-      const int d = valid ? (int)((key[k] >> a.shift) & dmask) : NB;
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
-      const int leader = __ffs(peers) - 1;
-      uint32_t old = 0;
-      if (valid && lane == leader) {
-        old = wcnt[warp * NB + d];
-        wcnt[warp * NB + d] = (uint16_t)(old + __popc(peers));
-      }
-      old = __shfl_sync(0xffffffffu, old, leader);
-      rank[k] = old + __popc(peers & lanemask_lt());
-      __syncwarp();
-    }
-    __syncthreads();
-    for (int d = tid; d < NB; d += NT) {
-      uint32_t acc = 0;
-#pragma unroll
-      for (int w2 = 0; w2 < NW; ++w2) {
-        const uint32_t c = wcnt[w2 * NB + d];
-        wcnt[w2 * NB + d] = (uint16_t)acc;
-        acc += c;
-      }
-      stot[d] = acc;
-    }
-    __syncthreads();
-    {
-      uint32_t sum = 0;
-      for (int j = 0; j < per; ++j) { const int d = tid * per + j; if (d < NB) sum += stot[d]; }
-      uint32_t tt;
-      uint32_t ex = block_excl_scan<NT, uint32_t>(sum, s_scan, &tt);
-      for (int j = 0; j < per; ++j) { const int d = tid * per + j; if (d < NB) { lstart[d] = ex; ex += stot[d]; } }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      const int idx = warp * 32 * IPT + k * 32 + lane;
-      if (idx < cnt) {
-        const int d = (int)((key[k] >> a.shift) & dmask);
-        sorted[lstart[d] + wcnt[warp * NB + d] + rank[k]] = key[k];
-      }
-    }
-    __syncthreads();
-    if (a.final_soa) {
-      for (int i = tid; i < cnt; i += NT) {
-        const uint64_t k = sorted[i];
-        const int d = (int)((k >> a.shift) & dmask);
-        const int64_t gp = ob + (int64_t)(offr[d] + (uint32_t)i - lstart[d]);
-        a.out_t[gp] = tb0 + (int64_t)(k >> kKeyPixBits);
-        a.out_x[gp] = (uint16_t)((k >> 1) & 0xffffu);
-        a.out_y[gp] = (uint16_t)((k >> 17) & 0xffffu);
-        a.out_p[gp] = (k & 1u) ? (int8_t)1 : (int8_t)-1;
-      }
-    } else {
-      for (int i = tid; i < cnt; i += NT) {
-        const uint64_t k = sorted[i];
-        const int d = (int)((k >> a.shift) & dmask);
-        a.keys_out[ob + (int64_t)(offr[d] + (uint32_t)i - lstart[d])] = k;
-      }
-    }
-    __syncthreads();
-    for (int d = tid; d < NB; d += NT) offr[d] += stot[d];
-    __syncthreads();
-  }
-}
-
-cudaError_t launch_group_order(const GroupOrderArgs& a, cudaStream_t st) {
-  const int NB = 1 << a.bits;
-  const size_t smem = (size_t)kOrdTile * 8 + (size_t)(kOrdThreads / 32) * NB * 2 + (size_t)NB * 12;
-  ensure_smem(k_group_order, smem);
-  dim3 grid(a.ngroups, a.nseg);
-  k_group_order<<<grid, kOrdThreads, smem, st>>>(a);
-  return cudaGetLastError();
-}
 
 }  // namespace evs
