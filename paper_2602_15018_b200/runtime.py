@@ -242,7 +242,7 @@ def d2h_rows(pool: PinnedPool, n: int, rows, stream=None):
     return [root[off:off + sz].view(np_dt[r.dtype]) for r, off, sz in zip(rows, offs, sizes)]
 
 
-def d2h_segments(pool: PinnedPool, counts, rows2d, stream=None):
+def d2h_segments(pool: PinnedPool, counts, rows2d, stream=None, sync: bool = True):
     """Device [nseg][cap] output pools -> host: the first counts[g] elements of
     every segment, packed per row into one pinned block (async copies, one
     synchronize).  Returns, per row, a list of per-segment numpy views."""
@@ -266,7 +266,8 @@ def d2h_segments(pool: PinnedPool, counts, rows2d, stream=None):
             views.append(root[base + e * es:base + (e + n) * es].view(np_dt[r.dtype]))
             e += n
         out.append(views)
-    (stream or torch.cuda.current_stream()).synchronize()
+    if sync:
+        (stream or torch.cuda.current_stream()).synchronize()
     return out
 
 

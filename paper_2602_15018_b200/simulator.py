@@ -162,6 +162,108 @@ class EventSimulator:
             out.append(row)
         return out
 
+    def run_host(self, windows, validate: bool = True):
+        """Pipelined host-buffer stepping: for each float32 numpy window
+        [S, T, H, W] of ``windows`` (ideally page-locked, see ``pin_host``)
+        yield the host EventBatch list [S][T] of that window, in order.
+
+        Window i+1's host->device copy and window i's device->host copy run on
+        their own streams while window i+1 computes; two output pools (two
+        engines sharing this simulator's state) let a window's results drain
+        while the next one is generated.  Results are views into pinned blocks
+        (valid while held).
+        """
+        import torch
+
+        from .events.types import EventBatch
+        from .runtime import PinnedPool, StepEngine, d2h_segments
+
+        assert self.engine is not None, "call reset() first"
+        dev = self.device
+        comp = torch.cuda.current_stream(dev)
+        h2d = torch.cuda.Stream(dev)
+        d2h = torch.cuda.Stream(dev)
+        if not hasattr(self, "_pool"):
+            self._pool = PinnedPool()
+        if not hasattr(self, "_engine2"):
+            self._engine2 = StepEngine(self.engine.shape, dev)
+        engines = [self.engine, self._engine2]
+        fbuf = [torch.empty((self.S, self.T, self.H, self.W), dtype=torch.float32, device=dev) for _ in range(2)]
+        ev_h2d = [torch.cuda.Event() for _ in range(2)]
+        ev_comp = [torch.cuda.Event() for _ in range(2)]
+        ev_d2h = [torch.cuda.Event() for _ in range(2)]
+        for e in ev_comp + ev_d2h:
+            e.record(comp)
+
+        def upload(i, win):
+            fr = np.ascontiguousarray(win, np.float32)
+            if fr.ndim == 3:
+                fr = fr[:, None]
+            with torch.cuda.stream(h2d):
+                h2d.wait_event(ev_comp[i % 2])  # window i-2 has finished reading this buffer
+                fbuf[i % 2].copy_(torch.from_numpy(fr), non_blocking=True)
+                ev_h2d[i % 2].record(h2d)
+
+        it = iter(windows)
+        win = next(it, None)
+        if win is None:
+            return
+        upload(0, win)
+        pending = None  # (batches, copy-done event) of the previous window
+        i = 0
+        while True:
+            eng = engines[i % 2]
+            comp.wait_event(ev_h2d[i % 2])
+            comp.wait_event(ev_d2h[i % 2])  # window i-2's results have left this pool
+            eng.launch(fbuf[i % 2], self.ref, self.last, self.thp, self.thn, t0=self.t_next, tick=self.tick,
+                       validate=validate, stream=comp)
+            ev_comp[i % 2].record(comp)
+            self.t_next += self.T * self.tick
+            self.step_index += 1
+            win = next(it, None)
+            if win is not None:
+                upload(i + 1, win)  # overlaps window i's compute and window i-1's drain
+            counts, dropped, res, bad = eng.fetch_info()  # waits for window i's compute
+            if bad != _lib.NO_BAD:
+                eng.reset_bad()
+                raise ValueError(f"invalid intensity in window {i} (flat index {int(bad)})")
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(ev_comp[i % 2])
+                t, x, y, p = d2h_segments(self._pool, counts, [eng.ev_t, eng.ev_x, eng.ev_y, eng.ev_p],
+                                          sync=False)
+                ev_d2h[i % 2].record(d2h)
+            dr = dropped.reshape(self.S, self.T)
+            batches = [[EventBatch(t=t[g].view(np.uint64), x=x[g].view(np.uint16), y=y[g].view(np.uint16),
+                                   polarity=p[g], dropped_count=int(dr[g // self.T, g % self.T]),
+                                   canonical=self.canonical)
+                        for g in range(s * self.T, (s + 1) * self.T)] for s in range(self.S)]
+            if pending is not None:
+                pending[1].synchronize()
+                yield pending[0]
+            pending = (batches, ev_d2h[i % 2])
+            if win is None:
+                pending[1].synchronize()
+                yield pending[0]
+                return
+            i += 1
+
+    @staticmethod
+    def pin_host(array: np.ndarray) -> np.ndarray:
+        """Page-lock a host numpy array in place (cudaHostRegister) so copies from
+        it run at full PCIe rate; returns the array.  Unpin with unpin_host."""
+        import torch
+
+        rc = torch.cuda.cudart().cudaHostRegister(array.ctypes.data, array.nbytes, 0)
+        if int(rc) != 0:
+            raise RuntimeError(f"cudaHostRegister failed ({int(rc)})")
+        return array
+
+    @staticmethod
+    def unpin_host(array: np.ndarray) -> None:
+        import torch
+
+        torch.cuda.cudart().cudaHostUnregister(array.ctypes.data)
+
     # -- CUDA graph replay -------------------------------------------------------
     def capture(self, frame_windows) -> None:
         """Capture one graph stepping through `frame_windows` ([S, T, H, W] each) in order."""

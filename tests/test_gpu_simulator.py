@@ -123,3 +123,35 @@ def test_step_host_matches_oracle():
                 ob = oracle.canonical_sort(oracle.generate(ost[s], frames[s, f], k * 1000, (k + 1) * 1000,
                                                            refractory_us=100))
                 assert out[s][f].same_events(ob), (step, s, f)
+
+
+def test_run_host_pipeline_matches_oracle():
+    """Pipelined host stepping (EventSimulator.run_host, pinned source windows)."""
+    import numpy as np
+
+    from paper_2602_15018_b200.simulator import EventSimulator
+
+    S, T, H, W = 2, 3, 36, 48
+    cfg = ev.EventCameraConfig(c_pos=0.15, c_neg=0.15, refractory_us=100)
+    sim = EventSimulator(W, H, streams=S, frames_per_step=T, config=cfg)
+    f0 = [texture_frame(W, H, 0.137 * s) for s in range(S)]
+    sim.reset(f0, seeds=list(range(S)))
+    ost = [oracle.init_state(f0[s], c_pos=0.15, c_neg=0.15, refractory_us=100, seed=s) for s in range(S)]
+    nwin = 5
+    wins = [np.stack([[texture_frame(W, H, 0.137 * s + 0.02 * (w * T + f + 1)) for f in range(T)]
+                      for s in range(S)]) for w in range(nwin)]
+    for w in wins:
+        EventSimulator.pin_host(w)
+    try:
+        got = list(sim.run_host(wins))
+    finally:
+        for w in wins:
+            EventSimulator.unpin_host(w)
+    assert len(got) == nwin
+    for w in range(nwin):
+        for s in range(S):
+            for f in range(T):
+                k = w * T + f
+                ob = oracle.canonical_sort(oracle.generate(ost[s], wins[w][s, f], k * 1000, (k + 1) * 1000,
+                                                           refractory_us=100))
+                assert got[w][s][f].same_events(ob), (w, s, f)
