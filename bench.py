@@ -356,7 +356,7 @@ def run_ours(args):
                 for j in range(max(1, PERIOD_FRAMES // math.gcd(T, PERIOD_FRAMES)))]
     for w in win_host:  # page-locked source windows (a renderer would write into these)
         EventSimulator.pin_host(w)
-    for _ in sim.run_host([win_host[j % len(win_host)] for j in range(2)]):
+    for _ in sim.run_host([win_host[j % len(win_host)] for j in range(4)]):  # (pinned pool warm)
         pass
     torch.cuda.synchronize()
     ke_steps = max(4, min(K, 40))
