@@ -39,7 +39,7 @@ struct StepLayout {
   int64_t max_tiles2, ovf_cap;
   size_t chunk_flag;
   size_t ctr, desc, zero2, region, tile_count, tile_ovf, tile_base, ovf_area, rows, tot, hist, gstart,
-      seg_tbase, seg_tile_prefix, status2, keysA, keysB, total;
+      seg_tbase, seg_tile_prefix, status2, keysA, keysB, total, bak_ref, bak_last;
   // fast canonical path (fast_path.cu)
   bool fast;
   int fG, fntiles, fnbk, fmaxp;
@@ -135,6 +135,8 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   L->keysB = off; off = align_up(off + (canon && L->npass > 1 ? ns * p->capacity * 8 : 0));
   const bool fast_sel = fast_shape(p, P, canon ? (p->max_dt > 0 ? p->max_dt : p->tick) : 0, &L->fG,
                                    &L->fntiles, &L->fnbk);
+  L->bak_ref = off; off = align_up(off + (fast_sel ? 0 : (size_t)p->streams * P * 4));
+  L->bak_last = off; off = align_up(off + (fast_sel ? 0 : (size_t)p->streams * P * 8));
   L->region = off; off = align_up(off + (fast_sel ? 0 : ns * nt * kTileCap * 8));
   L->ovf_area = off; off = align_up(off + (fast_sel ? 0 : ns * (size_t)L->ovf_cap * 8));
   L->fast = fast_shape(p, P, canon ? (p->max_dt > 0 ? p->max_dt : p->tick) : 0, &L->fG, &L->fntiles, &L->fnbk);
@@ -211,7 +213,10 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   int64_t* zero2 = at<int64_t>(ws, L.zero2);
 
   mark(0);
-  cudaError_t e = launch_prologue(b->frames, (int64_t)L.nseg * P, P, p->validate, b->bad_pixel,
+  // the tile-order path validates inside K1 (fused); the prologue then only
+  // zeroes the per-call counters and advances the device clock
+  const bool fuse_val = p->validate && !L.fast;
+  cudaError_t e = launch_prologue(b->frames, (int64_t)L.nseg * P, P, fuse_val ? 0 : p->validate, b->bad_pixel,
                                   b->reservations, L.nseg, desc, (int64_t)p->frames * p->tick, zero2,
                                   L.n2, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
@@ -297,6 +302,10 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   g.ovf_cursor = reinterpret_cast<unsigned long long*>(zero2);
   g.ovf_cap = L.ovf_cap;
   g.err = zero2 + L.nseg;
+  g.fuse_validate = fuse_val ? 1 : 0;
+  g.bad_rw = b->bad_pixel;
+  g.bak_ref = at<float>(ws, L.bak_ref);
+  g.bak_last = at<int64_t>(ws, L.bak_last);
   e = launch_generate(g, b->th_pos == nullptr, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(2);
@@ -309,6 +318,10 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   ts.ovf_cap = L.ovf_cap; ts.tile_base = at<int64_t>(ws, L.tile_base);
   ts.rows = g.rows; ts.tot = at<uint32_t>(ws, L.tot);
   ts.out_count = b->counts; ts.out_dropped = b->dropped; ts.bad = b->bad_pixel; ts.err = g.err;
+  if (fuse_val) {
+    ts.bak_ref = g.bak_ref; ts.bak_last = g.bak_last;
+    ts.ref = b->ref_log; ts.last = b->last_event_t; ts.sp = (int64_t)p->streams * P;
+  }
   e = launch_tilescan(ts, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(3);

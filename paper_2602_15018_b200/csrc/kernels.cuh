@@ -78,6 +78,14 @@ struct GenArgs {
   // same tile through chunk_flag[(s, tile)] = (launch << 8) | chunks_done
   int nchunks, tc;
   unsigned long long* chunk_flag;  // [S*ntiles]
+  // fused validation (model.py:28-39 semantics without a separate pass over the
+  // frames): K1 checks every value it loads (atomicMin of the first bad flat
+  // index), frame chunk 0 saves the call's initial state here, and k_tilescan
+  // restores it when some value was invalid (the state is then untouched).
+  int fuse_validate;
+  int64_t* bad_rw;
+  float* bak_ref;      // [S][P]
+  int64_t* bak_last;   // [S][P]
 };
 
 constexpr int kSlotsPerLane = 16;
@@ -99,6 +107,12 @@ struct TileScanArgs {
   const int64_t* bad;
   const int64_t* err;         // K1 overflow-area exhaustion -> out_dropped = -1
   int gt;
+  // fused validation: restore the state from the backup when a frame was invalid
+  const float* bak_ref;
+  const int64_t* bak_last;
+  float* ref;
+  int64_t* last;
+  int64_t sp;                 // S * P (0: no restore)
 };
 
 struct TileOrderArgs {
