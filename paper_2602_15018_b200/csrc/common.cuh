@@ -84,6 +84,27 @@ __device__ __forceinline__ T block_excl_scan(T v, T* smem, T* total) {
   return r;
 }
 
+// Block-wide exclusive scan with a single barrier: every thread sums the warp
+// totals itself.  `buf` (NT/32 elements) must not be rewritten before every
+// thread has returned (callers alternate buffers or have a barrier between).
+template <int NT, typename T>
+__device__ __forceinline__ T block_excl_scan_1s(T v, T* buf, T* total) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const T inc = warp_incl_scan(v);
+  if (lane == 31) buf[warp] = inc;
+  __syncthreads();
+  T pre = T(0), tot = T(0);
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const T x = buf[w];
+    pre += w < warp ? x : T(0);
+    tot += x;
+  }
+  *total = tot;
+  return pre + inc - v;
+}
+
 // Warp-cooperative decoupled lookback (called by a full warp).  `status`
 // points at the tile-status array of one chain; tile `t` has already
 // published its aggregate.  Returns the exclusive prefix for tile t.
