@@ -390,6 +390,12 @@ __global__ void __launch_bounds__(kFNT, kFCtasPerSm) k_fast_gen(FastArgs a) {
     if (f + 1 < a.T) load_frame(f + 1, vn4);
 
     // ---- 1. per pixel (rolled): lane math, state, crossings into the group lists ----
+    // each warp clears its own groups' bucket counters (no other warp touches
+    // them before this frame's barrier A)
+#pragma unroll
+    for (int k = 0; k < VPT; ++k)
+      for (int b = lane; b < nbk; b += 32) s_gc[(k * NW + warp) * KB + b] = 0;
+    __syncwarp();
     uint32_t chg = 0;
 #pragma unroll 1
     for (int k = 0; k < VPT; ++k) {
@@ -451,6 +457,7 @@ __global__ void __launch_bounds__(kFNT, kFCtasPerSm) k_fast_gen(FastArgs a) {
             const uint32_t peers = __match_any_sync(active, bk);
             if (lane == __ffs(peers) - 1) gc[bk] = (uint16_t)(gc[bk] + __popc(peers));
           }
+          __syncwarp();  // the next round's leader may update the same counter
         }
       }
     }
@@ -524,6 +531,7 @@ __global__ void __launch_bounds__(kFNT, kFCtasPerSm) k_fast_gen(FastArgs a) {
           bpos = __shfl_sync(active, bpos, leader);
           s_sorted[bpos + __popc(peers & lanemask_lt())] = key;
         }
+        __syncwarp();  // the next round's leader may update the same counter
       }
     }
     __syncthreads();  // C
@@ -537,8 +545,6 @@ __global__ void __launch_bounds__(kFNT, kFCtasPerSm) k_fast_gen(FastArgs a) {
       for (int i = 4 * n4 + tid; i < total; i += NT) dst[i] = s_sorted[i];
       uint32_t* rows = a.rows + (int64_t)seg * (nbk + 1) * a.ntiles + tile;
       for (int b = tid; b <= nbk; b += NT) rows[(int64_t)b * a.ntiles] = s_bstart[b];
-      if (tid < nbk)
-        for (int g = 0; g < NG; ++g) s_gc[g * KB + tid] = 0;
       if (tid == 0) {
         a.tile_src[st_idx] = kSrcSlot;
         if (s_res) atomicAdd(reinterpret_cast<unsigned long long*>(a.seg_res + seg), (unsigned long long)s_res);
