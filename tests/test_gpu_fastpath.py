@@ -91,17 +91,21 @@ def _texture_case(S, T, H, W, c, refr, sigma=0.0):
     return frames, ref0, last0, thp, thn
 
 
+PATHS = pytest.mark.parametrize("bucket", [True, False], ids=["bucket", "tile"])
+
+
+@PATHS
 @pytest.mark.parametrize("S,T,H,W,c,refr,sigma", [
     (1, 3, 720, 1280, 0.15, 100, 0.0),   # BASELINE config 2 shape
     (2, 4, 260, 346, 0.2, 0, 0.0),       # DAVIS
     (2, 3, 120, 160, 0.05, 0, 0.03),     # multi-crossing, non-uniform thresholds
     (1, 2, 33, 37, 0.1, 300, 0.0),       # ragged tiles, scalar loads
 ])
-def test_fast_matches_oracle(S, T, H, W, c, refr, sigma):
+def test_fast_matches_oracle(S, T, H, W, c, refr, sigma, bucket):
     frames, ref0, last0, thp, thn = _texture_case(S, T, H, W, c, refr, sigma)
     cap = 8 * H * W
     uniform = (c, c) if sigma == 0 else None
-    segs, ref, last = _run(frames, ref0, last0, thp, thn, refr, cap, uniform)
+    segs, ref, last = _run(frames, ref0, last0, thp, thn, refr, cap, uniform, legacy=not bucket)
     exp, oref, olast = _oracle_segments(frames, ref0, last0, thp, thn, refr, cap)
     _same(segs, exp)
     assert np.array_equal(ref, oref) and np.array_equal(last, olast)
@@ -158,26 +162,29 @@ def test_overflow_tiles_sorted_by_fixup():
         assert np.array_equal(ref, oref) and np.array_equal(last, olast)
 
 
+@PATHS
 @pytest.mark.parametrize("cap", [1, 777, 5000, 20000])
-def test_capacity_cut(cap):
+def test_capacity_cut(cap, bucket):
     frames, ref0, last0, thp, thn = _texture_case(2, 2, 96, 128, 0.05, 0)
-    segs, ref, last = _run(frames, ref0, last0, thp, thn, 0, cap, (0.05, 0.05))
+    segs, ref, last = _run(frames, ref0, last0, thp, thn, 0, cap, (0.05, 0.05), legacy=not bucket)
     exp, oref, olast = _oracle_segments(frames, ref0, last0, thp, thn, 0, cap)
     _same(segs, exp)
     assert np.array_equal(ref, oref) and np.array_equal(last, olast)
 
 
-def test_irregular_ticks_and_wide_dt():
+@PATHS
+def test_irregular_ticks_and_wide_dt(bucket):
     frames, ref0, last0, thp, thn = _texture_case(2, 3, 48, 80, 0.1, 200)
     tb = np.array([[0, 700, 2600, 2601], [50, 1100, 1400, 3400]], np.int64)
     segs, ref, last = _run(frames, ref0, last0, thp, thn, 200, 8 * 48 * 80, (0.1, 0.1), t_bounds=tb,
-                           max_dt=2048)
+                           max_dt=2048, legacy=not bucket)
     exp, oref, olast = _oracle_segments(frames, ref0, last0, thp, thn, 200, 8 * 48 * 80, t_bounds=tb)
     _same(segs, exp)
     assert np.array_equal(ref, oref) and np.array_equal(last, olast)
 
 
-def test_uniform_brightness_step_single_bucket():
+@PATHS
+def test_uniform_brightness_step_single_bucket(bucket):
     """Every pixel crosses at the same instant: one t_rel bucket holds all
     events (K2 multi-chunk path, K1 single-bucket ranking)."""
     H, W = 300, 400
@@ -188,7 +195,7 @@ def test_uniform_brightness_step_single_bucket():
     thp = np.full((1, H, W), 0.2, np.float32)
     thn = thp.copy()
     cap = 8 * H * W
-    segs, ref, last = _run(frames, ref0, last0, thp, thn, 0, cap, (0.2, 0.2))
+    segs, ref, last = _run(frames, ref0, last0, thp, thn, 0, cap, (0.2, 0.2), legacy=not bucket)
     exp, oref, olast = _oracle_segments(frames, ref0, last0, thp, thn, 0, cap)
     assert len(exp[0]) > 8192
     _same(segs, exp)
