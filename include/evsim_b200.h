@@ -17,6 +17,7 @@
  *   evs_accumulate      accumulate_events_to_image evsim/events/model.py:249-262
  *   evs_voxel           (no reference counterpart; repo-defined voxel grid)
  *   evs_limit_bandwidth limit_bandwidth           evsim/events/model.py:215-246
+ *   evs_render          render_pair               evsim/render.py:179-208 (frame producer)
  *   evs_seed_pcg64      numpy default_rng(seed) seeding used by
  *                       inject_noise_events (model.py:194) -- host only
  */
@@ -193,6 +194,33 @@ evs_status evs_selftest_log(int64_t n, const double* x, double* out_fast, double
  * words: little-endian u32 words of the non-negative seed.
  * out: state_hi, state_lo, inc_hi, inc_lo. */
 void evs_seed_pcg64(const uint32_t* words, int32_t nwords, uint64_t out[4]);
+
+
+/* GPU frame producer: render_pair of the reference
+ * (evsim/render.py:179-208) -- axis-aligned textured planes, pinhole camera,
+ * projective z-depth, misses -> ambient intensity / +inf depth.  `planes` is a
+ * DEVICE array; intensity / depth are device [H][W] f32 (depth may be NULL). */
+#define EVS_TEX_CHECKER 0 /* Checkerboard(cell, intensity_a, intensity_b), render.py:60-74 */
+#define EVS_TEX_NOISE 1   /* ValueNoise(scale, seed, lo, hi), render.py:78-108 */
+typedef struct evs_plane {
+  int32_t axis;      /* 0, 1, 2 */
+  int32_t kind;      /* EVS_TEX_* */
+  double offset;
+  double bounds[4];  /* amin, amax, bmin, bmax over the other two axes (ascending index) */
+  double cell;       /* checker cell size or noise scale */
+  double value_a;    /* intensity_a or lo */
+  double value_b;    /* intensity_b or hi */
+  uint64_t seed;     /* noise seed */
+} evs_plane;
+typedef struct evs_render_params {
+  int32_t width, height;
+  double fx, fy, cx, cy;
+  double rot[9];     /* world-from-body rotation, row-major (Pose.rotation_matrix) */
+  double origin[3];  /* camera position */
+  double ambient;
+} evs_render_params;
+evs_status evs_render(const evs_render_params* p, const evs_plane* planes, int32_t nplanes, float* intensity,
+                      float* depth, void* stream);
 
 #ifdef __cplusplus
 }

@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = (
     "evs_step_profiled", "evs_step_clock_init",
     "evs_sort_workspace_bytes", "evs_canonical_sort", "evs_batch_stats", "evs_seed_pcg64",
     "evs_noise_workspace_bytes", "evs_noise", "evs_accumulate", "evs_voxel",
-    "evs_limit_bandwidth_workspace_bytes", "evs_limit_bandwidth",
+    "evs_limit_bandwidth_workspace_bytes", "evs_limit_bandwidth", "evs_render",
 )
 
 
@@ -48,6 +48,22 @@ class StepParams(ctypes.Structure):
 
 
 EVS_FLAG_DEVICE_CLOCK = 1
+
+
+class RenderPlane(ctypes.Structure):  # evs_plane
+    _fields_ = [("axis", ctypes.c_int32), ("kind", ctypes.c_int32), ("offset", ctypes.c_double),
+                ("bounds", ctypes.c_double * 4), ("cell", ctypes.c_double), ("value_a", ctypes.c_double),
+                ("value_b", ctypes.c_double), ("seed", ctypes.c_uint64)]
+
+
+class RenderParams(ctypes.Structure):  # evs_render_params
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32), ("fx", ctypes.c_double),
+                ("fy", ctypes.c_double), ("cx", ctypes.c_double), ("cy", ctypes.c_double),
+                ("rot", ctypes.c_double * 9), ("origin", ctypes.c_double * 3), ("ambient", ctypes.c_double)]
+
+
+EVS_TEX_CHECKER = 0
+EVS_TEX_NOISE = 1
 
 
 class StepBuffers(ctypes.Structure):
@@ -131,6 +147,7 @@ def _bind_extras(L) -> None:
     L.evs_limit_bandwidth.argtypes = [i64, P, P, P, P, i64, i64, P, P, P, P, P, P, sz, P]
     L.evs_selftest_log.argtypes = [i64, P, P, P, P]
     L.evs_merge_canonical.argtypes = [i64, P, P, P, P, i64, P, P, P, P, i64, P, P, P, P, P, sz, P]
+    L.evs_render.argtypes = [ctypes.POINTER(RenderParams), P, i32, P, P, P]
 
 
 def check(rc: int, what: str) -> None:
