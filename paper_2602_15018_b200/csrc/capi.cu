@@ -102,11 +102,14 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   L->NB = canon ? (1 << L->bits) : 0;
   L->max_tiles2 = (canon && L->npass > 1) ? (p->capacity + kOrdTile - 1) / kOrdTile : 0;
   // tiles per histogram row / K2 CTA: as large as possible (fewer rows, longer
-  // K2 chunks) while keeping >= 2 K2 CTAs per SM over the whole batch
-  L->gt = 1;
-  while (L->gt < kMaxGroupTiles &&
-         (int64_t)((L->ntiles + 2 * L->gt - 1) / (2 * L->gt)) * L->nseg >= 2 * 148)
-    L->gt *= 2;
+  // K2 chunks) while keeping >= 1.5 K2 CTAs per SM over the whole batch (a
+  // single HD frame: 4 tiles -> 225 CTAs, inside one wave of 3 per SM)
+  {
+    const int64_t want = 3 * (int64_t)sm_count_current() / 2;
+    L->gt = 1;
+    for (int g = kMaxGroupTiles; g > 1; --g)
+      if ((int64_t)((L->ntiles + g - 1) / g) * L->nseg >= want) { L->gt = g; break; }
+  }
   L->ngroups = (L->ntiles + L->gt - 1) / L->gt;
   // overflow area (lanes with > kSlotsPerLane events): the kept events of a
   // frame never exceed the capacity, so capacity + one tile is always enough
@@ -135,8 +138,9 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   L->keysB = off; off = align_up(off + (canon && L->npass > 1 ? ns * p->capacity * 8 : 0));
   const bool fast_sel = fast_shape(p, P, canon ? (p->max_dt > 0 ? p->max_dt : p->tick) : 0, &L->fG,
                                    &L->fntiles, &L->fnbk);
-  L->bak_ref = off; off = align_up(off + (fast_sel ? 0 : (size_t)p->streams * P * 4));
-  L->bak_last = off; off = align_up(off + (fast_sel ? 0 : (size_t)p->streams * P * 8));
+  const bool bak = !fast_sel && p->frames >= 4;  // fused validation (step_impl)
+  L->bak_ref = off; off = align_up(off + (bak ? (size_t)p->streams * P * 4 : 0));
+  L->bak_last = off; off = align_up(off + (bak ? (size_t)p->streams * P * 8 : 0));
   L->region = off; off = align_up(off + (fast_sel ? 0 : ns * nt * kTileCap * 8));
   L->ovf_area = off; off = align_up(off + (fast_sel ? 0 : ns * (size_t)L->ovf_cap * 8));
   L->fast = fast_shape(p, P, canon ? (p->max_dt > 0 ? p->max_dt : p->tick) : 0, &L->fG, &L->fntiles, &L->fnbk);
@@ -213,9 +217,10 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   int64_t* zero2 = at<int64_t>(ws, L.zero2);
 
   mark(0);
-  // the tile-order path validates inside K1 (fused); the prologue then only
-  // zeroes the per-call counters and advances the device clock
-  const bool fuse_val = p->validate && !L.fast;
+  // the tile-order path validates inside K1 (fused: K1 backs up the state it
+  // overwrites, 12 B/px) when the call has >= 4 frames per stream; shorter calls
+  // read the frames once in the prologue (4 B/px per frame) instead
+  const bool fuse_val = p->validate && !L.fast && p->frames >= 4;
   cudaError_t e = launch_prologue(b->frames, (int64_t)L.nseg * P, P, fuse_val ? 0 : p->validate, b->bad_pixel,
                                   b->reservations, L.nseg, desc, (int64_t)p->frames * p->tick, zero2,
                                   L.n2, st);

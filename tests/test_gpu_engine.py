@@ -118,16 +118,17 @@ def test_graph_replay_matches_oracle():
     _check_segment(eng, 0, ob, 1)
 
 
-def test_invalid_frame_leaves_state_untouched():
+@pytest.mark.parametrize("T", [2, 5])  # prologue validation (T < 4) / fused into K1 (T >= 4)
+def test_invalid_frame_leaves_state_untouched(T):
     import torch
 
     H, W = 16, 24
-    frames, ost, ref, last, thp, thn, eng = _setup(2, 2, H, W, (0.2, 0.2), [0, 1])
+    frames, ost, ref, last, thp, thn, eng = _setup(2, T, H, W, (0.2, 0.2), [0, 1])
     frames[1, 1, 3, 5] = np.nan
     frames[1, 1, 7, 2] = 2.0
     ref0, last0 = ref.clone(), last.clone()
     eng.launch(torch.from_numpy(frames).cuda(), ref, last, t0=0, tick=1000)
     counts, dropped, res, bad = eng.fetch_info()
-    assert bad == (1 * 2 + 1) * H * W + 3 * W + 5
+    assert bad == (1 * T + 1) * H * W + 3 * W + 5
     assert torch.equal(ref, ref0) and torch.equal(last, last0)
     assert int(counts.sum()) == 0
