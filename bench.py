@@ -6,7 +6,8 @@ Workload (BASELINE.json configs[1]): HD 1280x720 camera, C=0.15, refractory
 time-ordered (t, x, y, p) output per frame.  A "step" is one evs_step over T
 consecutive frames of the camera (default T=50; every frame still gets its
 own canonical event segment); the same workload at one frame per launch (the
-reference's per-frame call granularity) is reported in "per_frame_launch".
+reference's per-frame call granularity) is reported in "per_frame_launch",
+canonical order and pixel-major (generate_events_serial) order.
 Frames cycle through a pre-generated ring of lcm(T, 50) frames (>= 184 MB >
 126 MB L2), so every step reads its frames from HBM.
 
@@ -193,9 +194,10 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def measure_t1(args, dev, cfg, phase0, rank):
+def measure_t1(args, dev, cfg, phase0, rank, order=None):
     """The same workload with one frame per launch (the reference's per-frame call
-    granularity), graph-replayed; reported next to the batched number."""
+    granularity), graph-replayed; reported next to the batched number.  order:
+    canonical (default) or pixel-major (generate_events_serial order, model.py:140)."""
     import torch
 
     from paper_2602_15018_b200 import _lib
@@ -206,7 +208,8 @@ def measure_t1(args, dev, cfg, phase0, rank):
     P = W * H
     ring = device_texture_ring(W, H, PERIOD_FRAMES, DRIFT, phase0, dev)
     st = ev.init_pixel_states(ev.IntensityFrame(W, H, 0, texture_frame(W, H, phase0)), cfg, seed=rank)
-    eng = StepEngine(StepShape(1, 1, H, W, 8 * P, _lib.EVS_ORDER_CANONICAL, TICK, cfg.log_eps, REFR,
+    order = _lib.EVS_ORDER_CANONICAL if order is None else order
+    eng = StepEngine(StepShape(1, 1, H, W, 8 * P, order, TICK, cfg.log_eps, REFR,
                                st.uniform_thresholds), dev)
     for k in range(5):
         eng.launch(ring[k:k + 1], st.d_ref_log, st.d_last_event_t, t0=k * TICK, tick=TICK)
@@ -414,7 +417,10 @@ def run_ours(args):
 
     per_frame = None
     if T != 1 and args.compare_t1:
+        from paper_2602_15018_b200 import _lib
+
         per_frame = measure_t1(args, dev, cfg, phase0, rank)
+        per_frame["pixel_major_order"] = measure_t1(args, dev, cfg, phase0, rank, _lib.EVS_ORDER_PIXEL_MAJOR)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

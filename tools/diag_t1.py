@@ -1,4 +1,4 @@
-"""Diagnostic: per-stage device times of one-frame steps (T=1), HD bench workload.
+"""Diagnostic (RES=WxH, ORDER=pixel|canonical pseudo-variables): per-stage device times of one-frame steps (T=1), HD bench workload.
 
   python tools/diag_t1.py [variant ...]    variant = ENV=VAL[,ENV=VAL] (e.g. EVS_GT=4)
 Per variant: stage times (events between stages) and back-to-back frame time.
@@ -15,18 +15,19 @@ from paper_2602_15018_b200 import _lib, events as ev
 from paper_2602_15018_b200.runtime import StepEngine, StepShape
 from paper_2602_15018_b200.synth import texture_frame
 
-W, H = 1280, 720
 dev = torch.device("cuda", 0)
-ring = bench.device_texture_ring(W, H, 50, 0.02, 0.0, dev)
 cfg = ev.EventCameraConfig(c_pos=0.15, c_neg=0.15, refractory_us=100)
 
 
 def run(variant):
     env = dict(kv.split("=", 1) for kv in variant.split(",") if kv)
+    W, H = map(int, env.pop("RES", "1280x720").split("x"))
+    order = _lib.EVS_ORDER_PIXEL_MAJOR if env.pop("ORDER", "canonical") == "pixel" else _lib.EVS_ORDER_CANONICAL
+    ring = bench.device_texture_ring(W, H, 50, 0.02, 0.0, dev)
     for k, v in env.items():
         os.environ[k] = v
     st = ev.init_pixel_states(ev.IntensityFrame(W, H, 0, texture_frame(W, H, 0.0)), cfg, seed=0)
-    eng = StepEngine(StepShape(1, 1, H, W, 8 * W * H, _lib.EVS_ORDER_CANONICAL, 1000, 0.01, 100,
+    eng = StepEngine(StepShape(1, 1, H, W, 8 * W * H, order, 1000, 0.01, 100,
                                st.uniform_thresholds), dev)
     rows = []
     k = 0
