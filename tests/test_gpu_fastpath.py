@@ -97,6 +97,7 @@ PATHS = pytest.mark.parametrize("bucket", [True, False], ids=["bucket", "tile"])
 @PATHS
 @pytest.mark.parametrize("S,T,H,W,c,refr,sigma", [
     (1, 3, 720, 1280, 0.15, 100, 0.0),   # BASELINE config 2 shape
+    (1, 1, 720, 1280, 0.15, 100, 0.0),   # one frame per call (4-tile groups, prologue validation)
     (2, 4, 260, 346, 0.2, 0, 0.0),       # DAVIS
     (2, 3, 120, 160, 0.05, 0, 0.03),     # multi-crossing, non-uniform thresholds
     (1, 2, 33, 37, 0.1, 300, 0.0),       # ragged tiles, scalar loads
