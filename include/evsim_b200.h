@@ -16,6 +16,7 @@
  *   evs_noise           inject_noise_events       evsim/events/model.py:174-212
  *   evs_accumulate      accumulate_events_to_image evsim/events/model.py:249-262
  *   evs_voxel           (no reference counterpart; repo-defined voxel grid)
+ *   evs_voxel_segments  the same over many device-counted segments (a window)
  *   evs_limit_bandwidth limit_bandwidth           evsim/events/model.py:215-246
  *   evs_render          render_pair               evsim/render.py:179-208 (frame producer)
  *   evs_seed_pcg64      numpy default_rng(seed) seeding used by
@@ -174,6 +175,21 @@ evs_status evs_voxel(int64_t n, const int64_t* t, const uint16_t* x, const uint1
                      const int8_t* p, int64_t t0, int64_t t1, int32_t bins, int32_t width,
                      int32_t height, float* out, void* workspace, size_t workspace_bytes,
                      void* stream);
+
+/* The same voxel grid over many event segments without a host round trip:
+ * segment s (s < nseg) holds counts[s * counts_stride] events (device int64)
+ * at element offset s * seg_stride of t/x/y/p -- the S x T rows of an evs_step
+ * output (counts = evs_step_buffers.counts, stride 1, seg_stride = capacity)
+ * or per-frame noise buffers (counts = meta[1], stride 4).  flags:
+ * EVS_VOXEL_CLEAR zeroes the int64 workspace first, EVS_VOXEL_FINALIZE rounds
+ * it into out; calls in between accumulate (signal + noise of one window). */
+#define EVS_VOXEL_CLEAR 1
+#define EVS_VOXEL_FINALIZE 2
+evs_status evs_voxel_segments(int32_t nseg, const int64_t* counts, int64_t counts_stride, int64_t seg_stride,
+                              const int64_t* t, const uint16_t* x, const uint16_t* y, const int8_t* p,
+                              int64_t t0, int64_t t1, int32_t bins, int32_t width, int32_t height,
+                              int32_t flags, float* out, void* workspace, size_t workspace_bytes,
+                              void* stream);
 
 /* limit_bandwidth (model.py:215-246) of a t-sorted device batch of n >= 1
  * events: keeps the first `cap` = int(rate * window * 1e-6) events of each

@@ -7,9 +7,10 @@
 //   evs_limit_bandwidth limit_bandwidth (model.py:215-246): keep the first
 //                       floor(rate * window) events of every window that
 //                       tiles forward from the first event.
-// The simulator path fuses the histogram / voxel accumulation into the
-// generate kernel (each lane owns its pixels, no atomics); these entry points
-// serve arbitrary batches and the noise events.
+//   evs_voxel_segments  the voxel grid over many device-counted segments (a
+//                       step's S x T output rows, per-frame noise buffers)
+//                       without a host round trip (EventSimulator.voxel_window).
+// All accumulate with global int64 atomics (exact, order independent).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -46,6 +47,37 @@ __global__ void __launch_bounds__(256) k_voxel_acc(int64_t n, const int64_t* __r
     const int64_t tau = (int64_t)(B - 1) * (ti - t0);
     const int64_t pix = (int64_t)y[i] * W + x[i];
     const int64_t b0 = tau / D;  // the two bins that can have weight > 0
+    for (int64_t b = b0; b <= b0 + 1 && b < B; ++b) {
+      int64_t d = b * D - tau;
+      d = d < 0 ? -d : d;
+      const int64_t w = D - d;
+      if (w > 0) atomicAdd(reinterpret_cast<unsigned long long*>(acc + b * P + pix),
+                           (unsigned long long)((int64_t)p[i] * w));
+    }
+  }
+}
+
+// the same numerators over many segments: segment s holds counts[s * cstride]
+// events at offset s * seg_stride (evs_step output rows, per-frame noise buffers)
+__global__ void __launch_bounds__(256) k_voxel_acc_seg(const int64_t* __restrict__ counts, int64_t cstride,
+                                                       int64_t seg_stride, const int64_t* __restrict__ t,
+                                                       const uint16_t* __restrict__ x,
+                                                       const uint16_t* __restrict__ y,
+                                                       const int8_t* __restrict__ p, int64_t t0, int64_t t1,
+                                                       int32_t B, int32_t W, int64_t P, long long* acc) {
+  const int64_t D = t1 - t0;
+  const int64_t seg = blockIdx.y;
+  int64_t n = counts[seg * cstride];
+  if (seg_stride > 0 && n > seg_stride) n = seg_stride;  // (an overflowed noise buffer: redone by the caller)
+  const int64_t base = seg * seg_stride;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + j;
+    const int64_t ti = t[i];
+    if (ti < t0 || ti >= t1) continue;
+    const int64_t tau = (int64_t)(B - 1) * (ti - t0);
+    const int64_t pix = (int64_t)y[i] * W + x[i];
+    if ((uint64_t)pix >= (uint64_t)P) continue;  // (bounds: the caller's segments are sensor events)
+    const int64_t b0 = tau / D;
     for (int64_t b = b0; b <= b0 + 1 && b < B; ++b) {
       int64_t d = b * D - tau;
       d = d < 0 ? -d : d;
@@ -163,6 +195,30 @@ evs_status evs_voxel(int64_t n, const int64_t* t, const uint16_t* x, const uint1
   if (cudaMemsetAsync(acc, 0, (size_t)bins * P * sizeof(long long), st) != cudaSuccess) return EVS_ERR_CUDA;
   if (n > 0) k_voxel_acc<<<grid_for(n, 148 * 16), 256, 0, st>>>(n, t, x, y, p, t0, t1, bins, width, P, acc);
   k_voxel_finalize<<<grid_for((int64_t)bins * P, 148 * 16), 256, 0, st>>>((int64_t)bins * P, acc, t1 - t0, out);
+  return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
+}
+
+evs_status evs_voxel_segments(int32_t nseg, const int64_t* counts, int64_t counts_stride, int64_t seg_stride,
+                              const int64_t* t, const uint16_t* x, const uint16_t* y, const int8_t* p,
+                              int64_t t0, int64_t t1, int32_t bins, int32_t width, int32_t height,
+                              int32_t flags, float* out, void* workspace, size_t ws_bytes, void* stream) {
+  if (nseg < 0 || nseg > 65535 || t1 <= t0 || bins < 2 || width < 1 || height < 1) return EVS_ERR_ARG;
+  if ((flags & EVS_VOXEL_FINALIZE) && !out) return EVS_ERR_ARG;
+  if (nseg > 0 && (!counts || !t || !x || !y || !p || seg_stride < 0 || counts_stride < 1)) return EVS_ERR_ARG;
+  const int64_t P = (int64_t)width * height;
+  if (!workspace || ws_bytes < (size_t)bins * P * sizeof(long long)) return EVS_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  long long* acc = static_cast<long long*>(workspace);
+  if ((flags & EVS_VOXEL_CLEAR) &&
+      cudaMemsetAsync(acc, 0, (size_t)bins * P * sizeof(long long), st) != cudaSuccess)
+    return EVS_ERR_CUDA;
+  if (nseg > 0) {
+    const int bx = (int)((148 * 8 + nseg - 1) / nseg);
+    k_voxel_acc_seg<<<dim3(bx < 4 ? 4 : bx, nseg), 256, 0, st>>>(counts, counts_stride, seg_stride, t, x, y, p,
+                                                               t0, t1, bins, width, P, acc);
+  }
+  if (flags & EVS_VOXEL_FINALIZE)
+    k_voxel_finalize<<<grid_for((int64_t)bins * P, 148 * 16), 256, 0, st>>>((int64_t)bins * P, acc, t1 - t0, out);
   return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
 }
 

@@ -300,6 +300,98 @@ class EventSimulator:
 
         return accumulate(batch, window_us, t_end, self.W, self.H, device_output=True)
 
+    def voxel_window(self, s: int = 0, bins: int = 5, noise_seeds=None, _noise_capacity=None):
+        """B-bin voxel grid, f32 (bins, H, W) on the device, of
+        stream s over the last step's window [t_next - T*tick, t_next): the
+        signal events of its T frames plus, when config.noise_rate_hz > 0 and
+        ``noise_seeds`` (one per frame) is given, the exact noise of every
+        frame (inject_noise_events, model.py:174-212, seeded per tick as
+        SimNode does, orchestrator.py:167-171).  The voxel sum is order
+        independent (exact int64 numerators, one rounding), so nothing is
+        sorted or merged: one segmented accumulation over the step's output
+        rows, T noise launches into a pooled buffer, one segmented accumulation
+        over it, one rounding, and one host read per window (the noise kernels'
+        retry flags; a flagged frame is redone by the retrying path)."""
+        import ctypes
+
+        import torch
+
+        from .noise import noise_params, run_noise
+
+        L = _lib.load()
+        e = self.engine
+        assert e is not None, "call reset() first"
+        T, W, H, P = self.T, self.W, self.H, self.P
+        t1 = self.t_next
+        t0 = t1 - T * self.tick
+        nbytes = int(L.evs_voxel_workspace_bytes(bins, W, H))
+        ws = getattr(self, "_vox_ws", None)
+        if ws is None or ws.numel() < nbytes:
+            ws = self._vox_ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        out = torch.empty((bins, H, W), dtype=torch.float32, device=self.device)
+        st = _lib.stream_ptr()
+        use_noise = self.cfg.noise_rate_hz > 0 and noise_seeds is not None
+        g0 = s * T
+
+        def vox(nseg, counts, cstride, sstride, t, x, y, p, flags):
+            rc = L.evs_voxel_segments(nseg, counts, cstride, sstride, t, x, y, p, t0, t1, bins, W, H, flags,
+                                      out.data_ptr(), ws.data_ptr(), ws.numel(), st)
+            _lib.check(rc, "evs_voxel_segments")
+
+        def signal(flags):
+            vox(T, e.info[0, g0:].data_ptr(), 1, e.ev_t.shape[1], e.ev_t[g0].data_ptr(), e.ev_x[g0].data_ptr(),
+                e.ev_y[g0].data_ptr(), e.ev_p[g0].data_ptr(), flags)
+
+        signal(_lib.EVS_VOXEL_CLEAR | (0 if use_noise else _lib.EVS_VOXEL_FINALIZE))
+        if not use_noise:
+            return out
+        seeds = list(noise_seeds)
+        if len(seeds) != T:
+            raise ValueError(f"need {T} noise seeds (one per frame), got {len(seeds)}")
+        params = [noise_params(W, H, t0 + f * self.tick, t0 + (f + 1) * self.tick, self.cfg.noise_rate_hz,
+                               seeds[f], order=0) for f in range(T)]
+        if params[0].lam <= 0:
+            vox(0, None, 1, 0, None, None, None, None, _lib.EVS_VOXEL_FINALIZE)
+            return out
+        cap = max(int(L.evs_noise_capacity(ctypes.byref(p))) for p in params)
+        if _noise_capacity is not None:
+            cap = int(_noise_capacity)
+        for p in params:
+            p.capacity = cap
+        nws = max(int(L.evs_noise_workspace_bytes(ctypes.byref(p))) for p in params)
+        pool = getattr(self, "_noise_pool", None)
+        if pool is None or pool["t"].shape[0] < T or pool["t"].shape[1] < cap or pool["ws"].numel() < nws:
+            pool = self._noise_pool = {
+                "t": torch.empty((T, cap), dtype=torch.int64, device=self.device),
+                "x": torch.empty((T, cap), dtype=torch.int16, device=self.device),
+                "y": torch.empty((T, cap), dtype=torch.int16, device=self.device),
+                "p": torch.empty((T, cap), dtype=torch.int8, device=self.device),
+                "meta": torch.zeros((T, 4), dtype=torch.int64, device=self.device),
+                "ws": torch.empty(max(nws, 1), dtype=torch.uint8, device=self.device)}
+        nt, nx, ny, npol, meta, nw = (pool[k] for k in ("t", "x", "y", "p", "meta", "ws"))
+        for f, p in enumerate(params):
+            rc = L.evs_noise(ctypes.byref(p), nt[f].data_ptr(), nx[f].data_ptr(), ny[f].data_ptr(),
+                             npol[f].data_ptr(), None, meta[f].data_ptr(), nw.data_ptr(), nw.numel(), st)
+            _lib.check(rc, "evs_noise")
+        stride = nt.shape[1]
+        vox(T, meta[:, 1].data_ptr(), 4, stride, nt.data_ptr(), nx.data_ptr(), ny.data_ptr(), npol.data_ptr(),
+            _lib.EVS_VOXEL_FINALIZE)
+        retry = meta[:T, 2:4].cpu().numpy()
+        if not retry.any():
+            return out
+        # rare: a frame's draw range or capacity was short -- redo the window with
+        # the retrying per-frame path (same result, noise_params rebuilt fresh)
+        signal(_lib.EVS_VOXEL_CLEAR)
+        for f in range(T):
+            p = noise_params(W, H, t0 + f * self.tick, t0 + (f + 1) * self.tick, self.cfg.noise_rate_hz,
+                             seeds[f], order=0)
+            n, b = run_noise(p, self.device)
+            cnt = torch.tensor([n], dtype=torch.int64, device=self.device)
+            vox(1, cnt.data_ptr(), 1, 0, b["t"].data_ptr(), b["x"].data_ptr(), b["y"].data_ptr(),
+                b["p"].data_ptr(), 0)
+        vox(0, None, 1, 0, None, None, None, None, _lib.EVS_VOXEL_FINALIZE)
+        return out
+
     def voxel(self, batch: DeviceEventBatch, t0: int, t1: int, bins: int = 5):
         from .represent import voxel_grid
 

@@ -155,3 +155,39 @@ def test_run_host_pipeline_matches_oracle():
                 ob = oracle.canonical_sort(oracle.generate(ost[s], wins[w][s, f], k * 1000, (k + 1) * 1000,
                                                            refractory_us=100))
                 assert got[w][s][f].same_events(ob), (w, s, f)
+
+
+@pytest.mark.parametrize("noise_cap", [None, 8])  # 8: every noise buffer overflows -> retrying path
+def test_voxel_window_signal_plus_noise_matches_oracle(noise_cap):
+    """EventSimulator.voxel_window: the T frames' signal events plus per-frame
+    exact noise of one window, accumulated without sorting / merging, equals
+    the oracle's voxel grid of the concatenated window batch."""
+    import torch
+
+    from paper_2602_15018_b200.simulator import EventSimulator, mix64
+
+    S, T, W, H = 2, 4, 160, 96
+    cfg = ev.EventCameraConfig(c_pos=0.05, c_neg=0.05, refractory_us=0, noise_rate_hz=2000.0)
+    sim = EventSimulator(W, H, streams=S, frames_per_step=T, config=cfg)
+    f0 = [texture_frame(W, H, 0.3 + 0.137 * s) for s in range(S)]
+    sim.reset(f0, seeds=[5 + s for s in range(S)])
+    ost = [oracle.init_state(f0[s], c_pos=0.05, c_neg=0.05, seed=5 + s) for s in range(S)]
+    k = 0
+    for step in range(2):
+        frames = np.stack([[texture_frame(W, H, 0.3 + 0.137 * s + 0.02 * (k + f + 1)) for f in range(T)]
+                           for s in range(S)])
+        sim.step(torch.from_numpy(frames).cuda())
+        for s in range(S):
+            seeds = [mix64(7 + s, 0x6E6F6973, k + f) for f in range(T)]
+            parts = []
+            for f in range(T):
+                t_prev, t_now = (k + f) * 1000, (k + f + 1) * 1000
+                parts.append(oracle.generate(ost[s], frames[s, f], t_prev, t_now))
+                parts.append(oracle.noise(W, H, t_prev, t_now, cfg.noise_rate_hz, seeds[f]))
+            exp = oracle.voxel(oracle.concat(parts), k * 1000, (k + T) * 1000, 5, W, H)
+            got = sim.voxel_window(s, bins=5, noise_seeds=seeds, _noise_capacity=noise_cap).cpu().numpy()
+            np.testing.assert_array_equal(got, exp)
+            sig_only = sim.voxel_window(s, bins=5).cpu().numpy()
+            exp_sig = oracle.voxel(oracle.concat(parts[0::2]), k * 1000, (k + T) * 1000, 5, W, H)
+            np.testing.assert_array_equal(sig_only, exp_sig)
+        k += T
