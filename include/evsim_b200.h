@@ -17,6 +17,7 @@
  *   evs_accumulate      accumulate_events_to_image evsim/events/model.py:249-262
  *   evs_voxel           (no reference counterpart; repo-defined voxel grid)
  *   evs_voxel_segments  the same over many device-counted segments (a window)
+ *   evs_step_voxel      the same from a step's per-tile regions (no atomics)
  *   evs_limit_bandwidth limit_bandwidth           evsim/events/model.py:215-246
  *   evs_render          render_pair               evsim/render.py:179-208 (frame producer)
  *   evs_seed_pcg64      numpy default_rng(seed) seeding used by
@@ -190,6 +191,18 @@ evs_status evs_voxel_segments(int32_t nseg, const int64_t* counts, int64_t count
                               int64_t t0, int64_t t1, int32_t bins, int32_t width, int32_t height,
                               int32_t flags, float* out, void* workspace, size_t workspace_bytes,
                               void* stream);
+
+/* Voxel grid of stream `stream_index` over [t0, t1) from the events of the
+ * last evs_step call made with these params / buffers / workspace (tile-order
+ * path): read from the step's per-tile key regions, one CTA per 1024-pixel
+ * tile accumulating its own pixels in shared memory (no global atomics).
+ * flags & EVS_VOXEL_FINALIZE: the f32 grid goes to out; otherwise the int64
+ * numerators are stored into voxel_ws (every pixel written: it replaces
+ * EVS_VOXEL_CLEAR) for evs_voxel_segments to add noise and finalize.  bins <= 24.
+ * EVS_ERR_UNSUPPORTED if the step ran the bucket path (EVS_PATH=bucket). */
+evs_status evs_step_voxel(const evs_step_params* p, const evs_step_buffers* b, const void* workspace,
+                          size_t workspace_bytes, int32_t stream_index, int64_t t0, int64_t t1, int32_t bins,
+                          int32_t flags, float* out, void* voxel_ws, size_t voxel_ws_bytes, void* stream);
 
 /* limit_bandwidth (model.py:215-246) of a t-sorted device batch of n >= 1
  * events: keeps the first `cap` = int(rate * window * 1e-6) events of each

@@ -139,6 +139,26 @@ struct TileOrderArgs {
   int gt;
 };
 
+// Voxel grid of one stream's window straight from a step's per-tile key
+// regions (represent.cu): one CTA per 1024-pixel tile accumulates the exact
+// int64 numerators of its own pixels in shared memory (no global atomics).
+struct StepVoxArgs {
+  int ntiles, T, s, B;
+  int W;
+  int64_t P, cap, ovf_cap;
+  const int64_t* tile_count;
+  const int64_t* tile_base;
+  const int64_t* tile_ovf;
+  const uint64_t* region;
+  const uint64_t* ovf_area;
+  const int64_t* seg_tbase;
+  const int64_t* bad;
+  int64_t t0, t1;
+  long long* acc_out;  // [B][P] int64 numerators (stored), or null
+  float* out;          // [B][P] f32 result, or null
+};
+constexpr int kStepVoxMaxBins = 24;
+cudaError_t launch_step_voxel(const StepVoxArgs& a, cudaStream_t st);
 cudaError_t launch_tilescan(const TileScanArgs& a, cudaStream_t st);
 cudaError_t launch_tile_order(const TileOrderArgs& a, cudaStream_t st);
 

@@ -60,8 +60,11 @@ struct NoiseArgs {
   double slam, loglam, pa, pb, log_invalpha, vr;
   uint64_t s_hi, s_lo, i_hi, i_lo;
   int64_t L, nthreads, cap;
-  int64_t* n_term;  // [nthreads] -> exclusive prefix after pass B
-  int64_t* n_ev;    // [nthreads] -> exclusive prefix after pass B
+  int64_t* n_term;  // [nthreads] per-walker counts (pass A)
+  int64_t* n_ev;    // [nthreads] per-walker counts (pass A)
+  int64_t* blk_term;  // [nblk] per-256-walker-block totals -> exclusive prefix (k_noise_scan)
+  int64_t* blk_ev;
+  int64_t nblk;
   int64_t* meta;    // [0] D (draws used by the counts) [1] total events [2] insufficient [3] overflow
   int32_t* ev_pix;  // [cap]
   int32_t* ev_trel; // [cap]
@@ -117,13 +120,12 @@ __device__ __forceinline__ int64_t ptrs_trial(const NoiseArgs& a, uint64_t u0, u
 // Walk thread c's part of the stream.  EMIT=false: count terminators/events.
 // EMIT=true: label events with pixels (needs the exclusive prefixes).
 template <bool EMIT>
-__global__ void __launch_bounds__(256) k_noise_walk(NoiseArgs a) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= a.nthreads) return;
+__device__ __forceinline__ void noise_walk_body(const NoiseArgs& a, int64_t c, int64_t term0, int64_t ev0,
+                                                int64_t& term, int64_t& ev) {
   const u128 inc = inc_of(a);
-  int64_t term = 0, ev = 0;
-  int64_t term0 = 0, ev0 = 0;
-  if (EMIT) { term0 = a.n_term[c]; ev0 = a.n_ev[c]; if (term0 >= a.P) return; }
+  term = 0;
+  ev = 0;
+  if (EMIT && term0 >= a.P) return;
   if (a.ptrs) {
     const int64_t m0 = c * a.L;
     u128 s = pcg_advance(s0_of(a), inc, (uint64_t)(2 * m0));
@@ -150,10 +152,7 @@ __global__ void __launch_bounds__(256) k_noise_walk(NoiseArgs a) {
     // skip to the first segment start owned by this thread
     if (c > 0) {
       for (;;) {
-        if (d >= d1) {  // no non-candidate in this chunk: an earlier thread owns it
-          if (!EMIT) { a.n_term[c] = 0; a.n_ev[c] = 0; }
-          return;
-        }
+        if (d >= d1) return;  // no non-candidate in this chunk: an earlier thread owns it
         s = s * pcg_mult() + inc;
         const double U = u_double(xsl_rr(s));
         ++d;
@@ -178,27 +177,87 @@ __global__ void __launch_bounds__(256) k_noise_walk(NoiseArgs a) {
       }
     }
   }
-  if (!EMIT) { a.n_term[c] = term; a.n_ev[c] = ev; }
 }
 
-// single-block exclusive scan of (n_term, n_ev); flags a too-short stream
-__global__ void __launch_bounds__(1024) k_noise_scan(NoiseArgs a) {
-  __shared__ int64_t s1[33], s2[33];
-  __shared__ int64_t run_t, run_e;
-  if (threadIdx.x == 0) { run_t = 0; run_e = 0; a.meta[0] = -1; a.meta[1] = 0; a.meta[2] = 0; a.meta[3] = 0; }
-  __syncthreads();
-  for (int64_t base = 0; base < a.nthreads; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    const int64_t t = i < a.nthreads ? a.n_term[i] : 0, e = i < a.nthreads ? a.n_ev[i] : 0;
+// Pass A (EMIT=false): per-walker counts and their per-block totals.  Pass B
+// (EMIT=true): each walker's exclusive prefix = block prefix (k_noise_scan)
+// + in-block scan, then the labelling walk.
+template <bool EMIT>
+__global__ void __launch_bounds__(256) k_noise_walk(NoiseArgs a) {
+  __shared__ int64_t s1[9], s2[9];
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool mine = c < a.nthreads;
+  int64_t term = 0, ev = 0;
+  if (!EMIT) {
+    if (mine) {
+      noise_walk_body<false>(a, c, 0, 0, term, ev);
+      a.n_term[c] = term;
+      a.n_ev[c] = ev;
+    }
     int64_t tt, te;
-    const int64_t xt = block_excl_scan<1024, int64_t>(t, s1, &tt);
-    const int64_t xe = block_excl_scan<1024, int64_t>(e, s2, &te);
-    if (i < a.nthreads) { a.n_term[i] = run_t + xt; a.n_ev[i] = run_e + xe; }
-    __syncthreads();
-    if (threadIdx.x == 0) { run_t += tt; run_e += te; }
-    __syncthreads();
+    block_excl_scan<256, int64_t>(term, s1, &tt);
+    block_excl_scan<256, int64_t>(ev, s2, &te);
+    if (threadIdx.x == 0) { a.blk_term[blockIdx.x] = tt; a.blk_ev[blockIdx.x] = te; }
+    return;
   }
-  if (threadIdx.x == 0 && run_t < a.P) a.meta[2] = 1;  // not enough draws: caller retries bigger
+  const int64_t rt = mine ? a.n_term[c] : 0, re = mine ? a.n_ev[c] : 0;
+  int64_t tt, te;
+  const int64_t t0 = block_excl_scan<256, int64_t>(rt, s1, &tt) + a.blk_term[blockIdx.x];
+  const int64_t e0 = block_excl_scan<256, int64_t>(re, s2, &te) + a.blk_ev[blockIdx.x];
+  if (mine) noise_walk_body<true>(a, c, t0, e0, term, ev);
+}
+
+// single-block exclusive scan of the walker-block totals (blk_term, blk_ev);
+// flags a too-short stream.  Chunks of kNsChunk blocks: coalesced loads into shared memory, each thread
+// sums its kNsPer consecutive entries, one block scan per array, prefixes
+// written back through shared memory with coalesced stores.
+constexpr int kNsPer = 4, kNsChunk = 1024 * kNsPer;
+__global__ void __launch_bounds__(1024) k_noise_scan(NoiseArgs a) {
+  extern __shared__ __align__(16) unsigned char nsm[];
+  int64_t* sT = reinterpret_cast<int64_t*>(nsm);  // [kNsChunk]
+  int64_t* sE = sT + kNsChunk;                    // [kNsChunk]
+  __shared__ int64_t s1[33], s2[33];
+  const int tid = threadIdx.x;
+  if (tid == 0) { a.meta[0] = -1; a.meta[1] = 0; a.meta[2] = 0; a.meta[3] = 0; }
+  const int64_t n = a.nblk;
+  int64_t run_t = 0, run_e = 0;
+  for (int64_t base = 0; base < n; base += kNsChunk) {
+#pragma unroll
+    for (int j = 0; j < kNsPer; ++j) {
+      const int64_t i = base + j * 1024 + tid;
+      sT[j * 1024 + tid] = i < n ? a.blk_term[i] : 0;
+      sE[j * 1024 + tid] = i < n ? a.blk_ev[i] : 0;
+    }
+    __syncthreads();
+    int64_t vt[kNsPer], ve[kNsPer], st = 0, se = 0;
+#pragma unroll
+    for (int j = 0; j < kNsPer; ++j) {
+      vt[j] = sT[tid * kNsPer + j];
+      ve[j] = sE[tid * kNsPer + j];
+      st += vt[j];
+      se += ve[j];
+    }
+    int64_t tt, te;
+    int64_t xt = block_excl_scan<1024, int64_t>(st, s1, &tt) + run_t;
+    int64_t xe = block_excl_scan<1024, int64_t>(se, s2, &te) + run_e;
+#pragma unroll
+    for (int j = 0; j < kNsPer; ++j) {
+      sT[tid * kNsPer + j] = xt;
+      sE[tid * kNsPer + j] = xe;
+      xt += vt[j];
+      xe += ve[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kNsPer; ++j) {
+      const int64_t i = base + j * 1024 + tid;
+      if (i < n) { a.blk_term[i] = sT[j * 1024 + tid]; a.blk_ev[i] = sE[j * 1024 + tid]; }
+    }
+    run_t += tt;
+    run_e += te;
+    __syncthreads();  // before the next chunk overwrites sT / sE
+  }
+  if (tid == 0 && run_t < a.P) a.meta[2] = 1;  // not enough draws: caller retries bigger
 }
 
 // per event: timestamp draw D + k and polarity byte k of the u32 stream
@@ -277,8 +336,8 @@ using namespace evs;
 namespace {
 
 struct NoiseLayout {
-  int64_t L, nthreads, cap;
-  size_t n_term, n_ev, meta, ev_pix, ev_trel, ev_pol, total;
+  int64_t L, nthreads, cap, nblk;
+  size_t n_term, n_ev, blk_term, blk_ev, meta, ev_pix, ev_trel, ev_pol, total;
 };
 
 constexpr size_t kAl = 256;
@@ -288,7 +347,7 @@ bool noise_layout(const evs_noise_params* p, NoiseLayout* L) {
   if (!p || p->width < 1 || p->height < 1 || p->t_now <= p->t_prev || !(p->lam > 0)) return false;
   const int64_t P = (int64_t)p->width * p->height;
   const bool ptrs = p->lam >= 10;
-  L->L = ptrs ? 32 : 64;
+  L->L = ptrs ? 32 : 64;  // draws per walker (16 measured no faster: the jump-ahead then dominates)
   // trials needed: P terminators; mult: P + events draws; PTRS: ~P/acceptance pairs
   const double mean_ev = p->lam * (double)P;
   const double draws = ptrs ? 1.5 * (double)P + 64.0 * std::sqrt((double)P) + 4096.0
@@ -299,6 +358,9 @@ bool noise_layout(const evs_noise_params* p, NoiseLayout* L) {
   size_t off = 0;
   L->n_term = off; off = al(off + (size_t)L->nthreads * 8);
   L->n_ev = off; off = al(off + (size_t)L->nthreads * 8);
+  L->nblk = (L->nthreads + 255) / 256;
+  L->blk_term = off; off = al(off + (size_t)L->nblk * 8);
+  L->blk_ev = off; off = al(off + (size_t)L->nblk * 8);
   L->meta = off; off = al(off + 8 * 8);
   L->ev_pix = off; off = al(off + (size_t)L->cap * 4);
   L->ev_trel = off; off = al(off + (size_t)L->cap * 4);
@@ -353,6 +415,9 @@ evs_status evs_noise(const evs_noise_params* p, int64_t* ev_t, uint16_t* ev_x, u
   a.L = L.L; a.nthreads = L.nthreads; a.cap = L.cap;
   a.n_term = at<int64_t>(ws, L.n_term);
   a.n_ev = at<int64_t>(ws, L.n_ev);
+  a.blk_term = at<int64_t>(ws, L.blk_term);
+  a.blk_ev = at<int64_t>(ws, L.blk_ev);
+  a.nblk = L.nblk;
   a.meta = meta_out ? meta_out : at<int64_t>(ws, L.meta);
   a.ev_pix = at<int32_t>(ws, L.ev_pix);
   a.ev_trel = at<int32_t>(ws, L.ev_trel);
@@ -361,7 +426,15 @@ evs_status evs_noise(const evs_noise_params* p, int64_t* ev_t, uint16_t* ev_x, u
   a.out_t = ev_t; a.out_x = ev_x; a.out_y = ev_y; a.out_p = ev_p; a.out_key = ev_key;
   const unsigned gw = (unsigned)((L.nthreads + 255) / 256);
   k_noise_walk<false><<<gw, 256, 0, st>>>(a);
-  k_noise_scan<<<1, 1024, 0, st>>>(a);
+  {
+    static bool raised = false;
+    const int smem = 2 * kNsChunk * (int)sizeof(int64_t);
+    if (!raised) {
+      cudaFuncSetAttribute(k_noise_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      raised = true;
+    }
+    k_noise_scan<<<1, 1024, smem, st>>>(a);
+  }
   k_noise_walk<true><<<gw, 256, 0, st>>>(a);
   const unsigned gd = (unsigned)((L.cap / 16 + 255) / 256 + 1);
   k_noise_draws<<<gd, 256, 0, st>>>(a);

@@ -34,6 +34,13 @@ __global__ void __launch_bounds__(256) k_accumulate(int64_t n, const int64_t* __
   }
 }
 
+// floor(tau / D) to within +-1 without a 64-bit integer division (tau, D <
+// 2^53 are exact doubles); the exact integer weight test below decides, so
+// scanning b0-1 .. b0+2 visits every bin with weight > 0
+__device__ __forceinline__ int64_t vox_bin_guess(int64_t tau, int64_t D) {
+  return (int64_t)((double)tau / (double)D);
+}
+
 // voxel numerators: acc[b][pix] += p * max(0, D - |b*D - (B-1)(t - t0)|)
 __global__ void __launch_bounds__(256) k_voxel_acc(int64_t n, const int64_t* __restrict__ t,
                                                    const uint16_t* __restrict__ x,
@@ -46,8 +53,8 @@ __global__ void __launch_bounds__(256) k_voxel_acc(int64_t n, const int64_t* __r
     if (ti < t0 || ti >= t1) continue;
     const int64_t tau = (int64_t)(B - 1) * (ti - t0);
     const int64_t pix = (int64_t)y[i] * W + x[i];
-    const int64_t b0 = tau / D;  // the two bins that can have weight > 0
-    for (int64_t b = b0; b <= b0 + 1 && b < B; ++b) {
+    const int64_t b0 = vox_bin_guess(tau, D);  // the bins with weight > 0 are among b0-1 .. b0+2
+    for (int64_t b = b0 > 0 ? b0 - 1 : 0; b <= b0 + 2 && b < B; ++b) {
       int64_t d = b * D - tau;
       d = d < 0 ? -d : d;
       const int64_t w = D - d;
@@ -77,8 +84,8 @@ __global__ void __launch_bounds__(256) k_voxel_acc_seg(const int64_t* __restrict
     const int64_t tau = (int64_t)(B - 1) * (ti - t0);
     const int64_t pix = (int64_t)y[i] * W + x[i];
     if ((uint64_t)pix >= (uint64_t)P) continue;  // (bounds: the caller's segments are sensor events)
-    const int64_t b0 = tau / D;
-    for (int64_t b = b0; b <= b0 + 1 && b < B; ++b) {
+    const int64_t b0 = vox_bin_guess(tau, D);
+    for (int64_t b = b0 > 0 ? b0 - 1 : 0; b <= b0 + 2 && b < B; ++b) {
       int64_t d = b * D - tau;
       d = d < 0 ? -d : d;
       const int64_t w = D - d;
@@ -94,6 +101,94 @@ __global__ void __launch_bounds__(256) k_voxel_finalize(int64_t m, const long lo
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (float)((double)acc[i] / (double)D);
   (void)inv;
+}
+
+// ---- voxel grid from a step's tile regions ---------------------------------
+// The kept events of (segment, tile) are the first nkeep keys of its region
+// (t_rel << 33 | y << 17 | x << 1 | p; capacity cut as in k_tile_order);
+// t = seg_tbase + t_rel.  One CTA per 1024-pixel tile accumulates its own
+// pixels' exact int64 numerators in shared memory (no global atomics); every
+// pixel of the tile is written, so the output needs no clearing.  When
+// (B-1)*D < 2^31 the bin arithmetic runs in 32 bits (exact floor by a float
+// guess and one integer correction).
+template <bool NARROW>
+__device__ __forceinline__ void vox_add(unsigned long long* acc, uint64_t k, int64_t tb, int64_t t0, int64_t t1,
+                                        int64_t D, float invD, int B, int W, int64_t tile0) {
+  const int64_t t = tb + (int64_t)(k >> kKeyPixBits);
+  if (t < t0 || t >= t1) return;
+  const int lp = (int)((int64_t)((k >> 17) & 0xffffu) * W + (int64_t)((k >> 1) & 0xffffu) - tile0);
+  const long long pol = (k & 1u) ? 1 : -1;
+  if (NARROW) {
+    const int d32 = (int)D;
+    const int tau = (B - 1) * (int)(t - t0);
+    int b0 = (int)((float)tau * invD);
+    if (b0 * d32 > tau) --b0;
+    else if ((b0 + 1) * d32 <= tau) ++b0;
+    for (int b = b0; b <= b0 + 1 && b < B; ++b) {
+      const int d = b * d32 - tau;
+      const int w = d32 - (d < 0 ? -d : d);
+      if (w > 0) atomicAdd(acc + b * kGenTile + lp, (unsigned long long)(pol * w));
+    }
+  } else {
+    const int64_t tau = (int64_t)(B - 1) * (t - t0);
+    const int64_t b0 = tau / D;
+    for (int64_t b = b0; b <= b0 + 1 && b < B; ++b) {
+      int64_t d = b * D - tau;
+      d = d < 0 ? -d : d;
+      const int64_t w = D - d;
+      if (w > 0) atomicAdd(acc + b * kGenTile + lp, (unsigned long long)(pol * w));
+    }
+  }
+}
+
+template <bool NARROW>
+__global__ void __launch_bounds__(256) k_step_voxel(StepVoxArgs a) {
+  extern __shared__ __align__(16) unsigned char vsm[];
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(vsm);  // [B][kGenTile]
+  const int q = blockIdx.x, tid = threadIdx.x;
+  for (int i = tid; i < a.B * kGenTile; i += blockDim.x) acc[i] = 0ull;
+  __syncthreads();
+  const int64_t D = a.t1 - a.t0;
+  const float invD = 1.0f / (float)D;
+  const int64_t tile0 = (int64_t)q * kGenTile;
+  if (*a.bad == kNoBad) {
+    for (int f = 0; f < a.T; ++f) {
+      const int64_t seg = (int64_t)a.s * a.T + f;
+      const int64_t sq = seg * a.ntiles + q;
+      const int64_t nq = a.tile_count[sq];
+      int64_t nkeep = a.cap - a.tile_base[sq];
+      nkeep = nkeep < 0 ? 0 : (nkeep > nq ? nq : nkeep);
+      const int64_t ov = a.tile_ovf[sq];
+      const uint64_t* src = ov >= 0 ? a.ovf_area + seg * a.ovf_cap + ov : a.region + sq * kTileCap;
+      const int64_t tb = a.seg_tbase[seg];
+      for (int64_t i = tid; i < nkeep; i += blockDim.x)
+        vox_add<NARROW>(acc, __ldcs(src + i), tb, a.t0, a.t1, D, invD, a.B, a.W, tile0);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < a.B * kGenTile; i += blockDim.x) {
+    const int b = i / kGenTile, lp = i % kGenTile;
+    const int64_t pix = tile0 + lp;
+    if (pix >= a.P) continue;
+    const long long v = (long long)acc[i];
+    if (a.out) a.out[(int64_t)b * a.P + pix] = (float)((double)v / (double)D);  // = k_voxel_finalize
+    else a.acc_out[(int64_t)b * a.P + pix] = v;
+  }
+}
+
+cudaError_t launch_step_voxel(const StepVoxArgs& a, cudaStream_t st) {
+  const size_t smem = (size_t)a.B * kGenTile * sizeof(long long);
+  static bool raised = false;
+  if (!raised) {
+    const int mx = (int)((size_t)kStepVoxMaxBins * kGenTile * sizeof(long long));
+    cudaFuncSetAttribute(k_step_voxel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_step_voxel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    raised = true;
+  }
+  const bool narrow = (int64_t)(a.B - 1) * (a.t1 - a.t0) < (1ll << 30);
+  if (narrow) k_step_voxel<true><<<a.ntiles, 256, smem, st>>>(a);
+  else k_step_voxel<false><<<a.ntiles, 256, smem, st>>>(a);
+  return cudaGetLastError();
 }
 
 // ---- limit_bandwidth -------------------------------------------------------

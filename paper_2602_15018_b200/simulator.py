@@ -308,10 +308,12 @@ class EventSimulator:
         frame (inject_noise_events, model.py:174-212, seeded per tick as
         SimNode does, orchestrator.py:167-171).  The voxel sum is order
         independent (exact int64 numerators, one rounding), so nothing is
-        sorted or merged: one segmented accumulation over the step's output
-        rows, T noise launches into a pooled buffer, one segmented accumulation
-        over it, one rounding, and one host read per window (the noise kernels'
-        retry flags; a flagged frame is redone by the retrying path)."""
+        sorted or merged: the signal numerators come straight from the step's
+        per-tile key regions (evs_step_voxel: one CTA per tile, shared-memory
+        accumulation; the bucket path uses its output rows), T noise launches
+        fill a pooled buffer, one segmented accumulation adds the noise, one
+        rounding, and one host read per window (the noise kernels' retry
+        flags; a flagged frame is redone by the retrying path)."""
         import ctypes
 
         import torch
@@ -339,10 +341,20 @@ class EventSimulator:
             _lib.check(rc, "evs_voxel_segments")
 
         def signal(flags):
-            vox(T, e.info[0, g0:].data_ptr(), 1, e.ev_t.shape[1], e.ev_t[g0].data_ptr(), e.ev_x[g0].data_ptr(),
-                e.ev_y[g0].data_ptr(), e.ev_p[g0].data_ptr(), flags)
+            # from the step's per-tile regions (shared-memory accumulation, every
+            # pixel written); the bucket path has none: the output rows instead
+            fin = flags & _lib.EVS_VOXEL_FINALIZE
+            rc = L.evs_step_voxel(ctypes.byref(e.params), ctypes.byref(e.bufs), e.workspace.data_ptr(),
+                                  e.workspace.numel(), s, t0, t1, bins, fin, out.data_ptr(), ws.data_ptr(),
+                                  ws.numel(), st)
+            if rc == _lib.EVS_ERR_UNSUPPORTED:
+                vox(T, e.info[0, g0:].data_ptr(), 1, e.ev_t.shape[1], e.ev_t[g0].data_ptr(),
+                    e.ev_x[g0].data_ptr(), e.ev_y[g0].data_ptr(), e.ev_p[g0].data_ptr(),
+                    flags | _lib.EVS_VOXEL_CLEAR)
+            else:
+                _lib.check(rc, "evs_step_voxel")
 
-        signal(_lib.EVS_VOXEL_CLEAR | (0 if use_noise else _lib.EVS_VOXEL_FINALIZE))
+        signal(0 if use_noise else _lib.EVS_VOXEL_FINALIZE)
         if not use_noise:
             return out
         seeds = list(noise_seeds)
@@ -381,7 +393,7 @@ class EventSimulator:
             return out
         # rare: a frame's draw range or capacity was short -- redo the window with
         # the retrying per-frame path (same result, noise_params rebuilt fresh)
-        signal(_lib.EVS_VOXEL_CLEAR)
+        signal(0)
         for f in range(T):
             p = noise_params(W, H, t0 + f * self.tick, t0 + (f + 1) * self.tick, self.cfg.noise_rate_hz,
                              seeds[f], order=0)

@@ -157,8 +157,10 @@ def test_run_host_pipeline_matches_oracle():
                 assert got[w][s][f].same_events(ob), (w, s, f)
 
 
-@pytest.mark.parametrize("noise_cap", [None, 8])  # 8: every noise buffer overflows -> retrying path
-def test_voxel_window_signal_plus_noise_matches_oracle(noise_cap):
+@pytest.mark.parametrize("noise_cap,path,canonical", [
+    (None, "tile", True), (8, "tile", True),   # 8: every noise buffer overflows -> retrying path
+    (None, "tile", False), (None, "bucket", True)])
+def test_voxel_window_signal_plus_noise_matches_oracle(noise_cap, path, canonical, monkeypatch):
     """EventSimulator.voxel_window: the T frames' signal events plus per-frame
     exact noise of one window, accumulated without sorting / merging, equals
     the oracle's voxel grid of the concatenated window batch."""
@@ -166,9 +168,11 @@ def test_voxel_window_signal_plus_noise_matches_oracle(noise_cap):
 
     from paper_2602_15018_b200.simulator import EventSimulator, mix64
 
+    if path == "bucket":
+        monkeypatch.setenv("EVS_PATH", "bucket")
     S, T, W, H = 2, 4, 160, 96
     cfg = ev.EventCameraConfig(c_pos=0.05, c_neg=0.05, refractory_us=0, noise_rate_hz=2000.0)
-    sim = EventSimulator(W, H, streams=S, frames_per_step=T, config=cfg)
+    sim = EventSimulator(W, H, streams=S, frames_per_step=T, config=cfg, canonical=canonical)
     f0 = [texture_frame(W, H, 0.3 + 0.137 * s) for s in range(S)]
     sim.reset(f0, seeds=[5 + s for s in range(S)])
     ost = [oracle.init_state(f0[s], c_pos=0.05, c_neg=0.05, seed=5 + s) for s in range(S)]
@@ -191,3 +195,22 @@ def test_voxel_window_signal_plus_noise_matches_oracle(noise_cap):
             exp_sig = oracle.voxel(oracle.concat(parts[0::2]), k * 1000, (k + T) * 1000, 5, W, H)
             np.testing.assert_array_equal(sig_only, exp_sig)
         k += T
+
+
+def test_voxel_window_wide_window_64bit_bins():
+    """(B-1) * window >= 2^30 us: the 64-bit bin arithmetic of evs_step_voxel."""
+    import torch
+
+    from paper_2602_15018_b200.simulator import EventSimulator
+
+    T, W, H, tick = 2, 96, 64, 300_000_000
+    cfg = ev.EventCameraConfig(c_pos=0.1, c_neg=0.1, refractory_us=0)
+    sim = EventSimulator(W, H, streams=1, frames_per_step=T, config=cfg, tick_us=tick)
+    f0 = texture_frame(W, H, 0.2)
+    sim.reset([f0], seeds=[3])
+    ost = oracle.init_state(f0, c_pos=0.1, c_neg=0.1, seed=3)
+    frames = np.stack([[texture_frame(W, H, 0.2 + 0.03 * (f + 1)) for f in range(T)]])
+    sim.step(torch.from_numpy(frames).cuda())
+    parts = [oracle.generate(ost, frames[0, f], f * tick, (f + 1) * tick) for f in range(T)]
+    exp = oracle.voxel(oracle.concat(parts), 0, T * tick, 5, W, H)
+    np.testing.assert_array_equal(sim.voxel_window(0, bins=5).cpu().numpy(), exp)
