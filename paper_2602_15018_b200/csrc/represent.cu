@@ -107,62 +107,105 @@ __global__ void __launch_bounds__(256) k_voxel_finalize(int64_t m, const long lo
 // The kept events of (segment, tile) are the first nkeep keys of its region
 // (t_rel << 33 | y << 17 | x << 1 | p; capacity cut as in k_tile_order);
 // t = seg_tbase + t_rel.  One CTA per 1024-pixel tile accumulates its own
-// pixels' exact int64 numerators in shared memory (no global atomics); every
-// pixel of the tile is written, so the output needs no clearing.  When
-// (B-1)*D < 2^31 the bin arithmetic runs in 32 bits (exact floor by a float
-// guess and one integer correction).
-template <bool NARROW>
-__device__ __forceinline__ void vox_add(unsigned long long* acc, uint64_t k, int64_t tb, int64_t t0, int64_t t1,
-                                        int64_t D, float invD, int B, int W, int64_t tile0) {
-  const int64_t t = tb + (int64_t)(k >> kKeyPixBits);
-  if (t < t0 || t >= t1) return;
-  const int lp = (int)((int64_t)((k >> 17) & 0xffffu) * W + (int64_t)((k >> 1) & 0xffffu) - tile0);
-  const long long pol = (k & 1u) ? 1 : -1;
-  if (NARROW) {
-    const int d32 = (int)D;
-    const int tau = (B - 1) * (int)(t - t0);
-    int b0 = (int)((float)tau * invD);
-    if (b0 * d32 > tau) --b0;
-    else if ((b0 + 1) * d32 <= tau) ++b0;
-    for (int b = b0; b <= b0 + 1 && b < B; ++b) {
-      const int d = b * d32 - tau;
-      const int w = d32 - (d < 0 ? -d : d);
-      if (w > 0) atomicAdd(acc + b * kGenTile + lp, (unsigned long long)(pol * w));
-    }
-  } else {
-    const int64_t tau = (int64_t)(B - 1) * (t - t0);
-    const int64_t b0 = tau / D;
-    for (int64_t b = b0; b <= b0 + 1 && b < B; ++b) {
-      int64_t d = b * D - tau;
-      d = d < 0 ? -d : d;
-      const int64_t w = D - d;
-      if (w > 0) atomicAdd(acc + b * kGenTile + lp, (unsigned long long)(pol * w));
-    }
-  }
+// pixels' exact numerators in shared memory (no global atomics); every pixel
+// of the tile is written, so the output needs no clearing.
+//   NARROW ((B-1) * D < 2^30): 32-bit bin arithmetic and 32-bit shared
+//   atomics, plus a per-pixel event count; a tile where count * D could reach
+//   2^31 (never at camera rates) is redone with the 64-bit accumulators.
+//   wide: 64-bit arithmetic and 64-bit shared atomics throughout.
+struct VoxTileSrc {
+  const uint64_t* src;
+  int64_t nkeep, tb;
+};
+__device__ __forceinline__ VoxTileSrc vox_tile_src(const StepVoxArgs& a, int q, int f) {
+  const int64_t seg = (int64_t)a.s * a.T + f;
+  const int64_t sq = seg * a.ntiles + q;
+  const int64_t nq = a.tile_count[sq];
+  int64_t nkeep = a.cap - a.tile_base[sq];
+  nkeep = nkeep < 0 ? 0 : (nkeep > nq ? nq : nkeep);
+  const int64_t ov = a.tile_ovf[sq];
+  VoxTileSrc r;
+  r.src = ov >= 0 ? a.ovf_area + seg * a.ovf_cap + ov : a.region + sq * kTileCap;
+  r.nkeep = nkeep;
+  r.tb = a.seg_tbase[seg];
+  return r;
 }
 
-template <bool NARROW>
-__global__ void __launch_bounds__(256) k_step_voxel(StepVoxArgs a) {
+__global__ void __launch_bounds__(256) k_step_voxel(StepVoxArgs a, int narrow) {
   extern __shared__ __align__(16) unsigned char vsm[];
-  unsigned long long* acc = reinterpret_cast<unsigned long long*>(vsm);  // [B][kGenTile]
   const int q = blockIdx.x, tid = threadIdx.x;
+  const int64_t D = a.t1 - a.t0;
+  const int64_t tile0 = (int64_t)q * kGenTile;
+  const bool ok = *a.bad == kNoBad;
+  __shared__ int s_wide;
+  if (narrow) {
+    int* acc = reinterpret_cast<int*>(vsm);        // [B][kGenTile]
+    int* cnt = acc + a.B * kGenTile;               // [kGenTile]
+    for (int i = tid; i < (a.B + 1) * kGenTile; i += blockDim.x) acc[i] = 0;
+    if (tid == 0) s_wide = 0;
+    __syncthreads();
+    const int d32 = (int)D;
+    const float invD = 1.0f / (float)D;
+    if (ok) {
+      for (int f = 0; f < a.T; ++f) {
+        const VoxTileSrc r = vox_tile_src(a, q, f);
+        for (int64_t i = tid; i < r.nkeep; i += blockDim.x) {
+          const uint64_t k = __ldcs(r.src + i);
+          const int64_t t = r.tb + (int64_t)(k >> kKeyPixBits);
+          if (t < a.t0 || t >= a.t1) continue;
+          const int lp = (int)((int64_t)((k >> 17) & 0xffffu) * a.W + (int64_t)((k >> 1) & 0xffffu) - tile0);
+          const int pol = (k & 1u) ? 1 : -1;
+          const int tau = (a.B - 1) * (int)(t - a.t0);
+          int b0 = (int)((float)tau * invD);  // floor(tau / D) within +-1, corrected below
+          if (b0 * d32 > tau) --b0;
+          else if ((b0 + 1) * d32 <= tau) ++b0;
+          atomicAdd(cnt + lp, 1);
+          for (int b = b0; b <= b0 + 1 && b < a.B; ++b) {
+            const int d = b * d32 - tau;
+            const int w = d32 - (d < 0 ? -d : d);
+            if (w > 0) atomicAdd(acc + b * kGenTile + lp, pol * w);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < kGenTile; i += blockDim.x)
+      if ((int64_t)cnt[i] * D >= (1ll << 31)) s_wide = 1;
+    __syncthreads();
+    if (!s_wide) {
+      for (int i = tid; i < a.B * kGenTile; i += blockDim.x) {
+        const int b = i / kGenTile, lp = i % kGenTile;
+        const int64_t pix = tile0 + lp;
+        if (pix >= a.P) continue;
+        const long long v = acc[i];
+        if (a.out) a.out[(int64_t)b * a.P + pix] = (float)((double)v / (double)D);  // = k_voxel_finalize
+        else a.acc_out[(int64_t)b * a.P + pix] = v;
+      }
+      return;
+    }
+    __syncthreads();  // (redo this tile below with 64-bit accumulators)
+  }
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(vsm);  // [B][kGenTile]
   for (int i = tid; i < a.B * kGenTile; i += blockDim.x) acc[i] = 0ull;
   __syncthreads();
-  const int64_t D = a.t1 - a.t0;
-  const float invD = 1.0f / (float)D;
-  const int64_t tile0 = (int64_t)q * kGenTile;
-  if (*a.bad == kNoBad) {
+  if (ok) {
     for (int f = 0; f < a.T; ++f) {
-      const int64_t seg = (int64_t)a.s * a.T + f;
-      const int64_t sq = seg * a.ntiles + q;
-      const int64_t nq = a.tile_count[sq];
-      int64_t nkeep = a.cap - a.tile_base[sq];
-      nkeep = nkeep < 0 ? 0 : (nkeep > nq ? nq : nkeep);
-      const int64_t ov = a.tile_ovf[sq];
-      const uint64_t* src = ov >= 0 ? a.ovf_area + seg * a.ovf_cap + ov : a.region + sq * kTileCap;
-      const int64_t tb = a.seg_tbase[seg];
-      for (int64_t i = tid; i < nkeep; i += blockDim.x)
-        vox_add<NARROW>(acc, __ldcs(src + i), tb, a.t0, a.t1, D, invD, a.B, a.W, tile0);
+      const VoxTileSrc r = vox_tile_src(a, q, f);
+      for (int64_t i = tid; i < r.nkeep; i += blockDim.x) {
+        const uint64_t k = __ldcs(r.src + i);
+        const int64_t t = r.tb + (int64_t)(k >> kKeyPixBits);
+        if (t < a.t0 || t >= a.t1) continue;
+        const int lp = (int)((int64_t)((k >> 17) & 0xffffu) * a.W + (int64_t)((k >> 1) & 0xffffu) - tile0);
+        const long long pol = (k & 1u) ? 1 : -1;
+        const int64_t tau = (int64_t)(a.B - 1) * (t - a.t0);
+        const int64_t b0 = tau / D;
+        for (int64_t b = b0; b <= b0 + 1 && b < a.B; ++b) {
+          int64_t d = b * D - tau;
+          d = d < 0 ? -d : d;
+          const int64_t w = D - d;
+          if (w > 0) atomicAdd(acc + b * kGenTile + lp, (unsigned long long)(pol * w));
+        }
+      }
     }
   }
   __syncthreads();
@@ -177,17 +220,15 @@ __global__ void __launch_bounds__(256) k_step_voxel(StepVoxArgs a) {
 }
 
 cudaError_t launch_step_voxel(const StepVoxArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)a.B * kGenTile * sizeof(long long);
+  const size_t smem = (size_t)a.B * kGenTile * sizeof(long long);  // >= the narrow (B + 1) x 4 B
   static bool raised = false;
   if (!raised) {
-    const int mx = (int)((size_t)kStepVoxMaxBins * kGenTile * sizeof(long long));
-    cudaFuncSetAttribute(k_step_voxel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_step_voxel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_step_voxel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((size_t)kStepVoxMaxBins * kGenTile * sizeof(long long)));
     raised = true;
   }
-  const bool narrow = (int64_t)(a.B - 1) * (a.t1 - a.t0) < (1ll << 30);
-  if (narrow) k_step_voxel<true><<<a.ntiles, 256, smem, st>>>(a);
-  else k_step_voxel<false><<<a.ntiles, 256, smem, st>>>(a);
+  const int narrow = (int64_t)(a.B - 1) * (a.t1 - a.t0) < (1ll << 30) ? 1 : 0;
+  k_step_voxel<<<a.ntiles, 256, smem, st>>>(a, narrow);
   return cudaGetLastError();
 }
 
