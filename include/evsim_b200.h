@@ -18,6 +18,7 @@
  *   evs_voxel           (no reference counterpart; repo-defined voxel grid)
  *   evs_voxel_segments  the same over many device-counted segments (a window)
  *   evs_step_voxel      the same from a step's per-tile regions (no atomics)
+ *   evs_step_histogram  accumulate_events_to_image of every stream of a step
  *   evs_limit_bandwidth limit_bandwidth           evsim/events/model.py:215-246
  *   evs_render          render_pair               evsim/render.py:179-208 (frame producer)
  *   evs_seed_pcg64      numpy default_rng(seed) seeding used by
@@ -203,6 +204,15 @@ evs_status evs_voxel_segments(int32_t nseg, const int64_t* counts, int64_t count
 evs_status evs_step_voxel(const evs_step_params* p, const evs_step_buffers* b, const void* workspace,
                           size_t workspace_bytes, int32_t stream_index, int64_t t0, int64_t t1, int32_t bins,
                           int32_t flags, float* out, void* voxel_ws, size_t voxel_ws_bytes, void* stream);
+
+/* accumulate_events_to_image (model.py:249-262) of EVERY stream of the last
+ * evs_step call on this workspace: out[s][y][x] (int64, device) = sum of the
+ * polarities of stream s's events with t in [t_end - window_us, t_end), read
+ * from the step's per-tile regions in one launch (tile-order path;
+ * EVS_ERR_UNSUPPORTED after the bucket path). */
+evs_status evs_step_histogram(const evs_step_params* p, const evs_step_buffers* b, const void* workspace,
+                              size_t workspace_bytes, int64_t window_us, int64_t t_end, int64_t* out,
+                              void* stream);
 
 /* limit_bandwidth (model.py:215-246) of a t-sorted device batch of n >= 1
  * events: keeps the first `cap` = int(rate * window * 1e-6) events of each

@@ -404,6 +404,21 @@ evs_status evs_selftest_log(int64_t n, const double* x, double* out_fast, double
              ? EVS_OK : EVS_ERR_CUDA;
 }
 
+static void step_regions(const evs_step_params* p, const evs_step_buffers* b, const StepLayout& L, const void* ws,
+                         StepVoxArgs* a) {
+  memset(a, 0, sizeof(*a));
+  a->ntiles = L.ntiles; a->T = p->frames; a->W = p->width;
+  a->P = (int64_t)p->height * p->width; a->cap = p->capacity; a->ovf_cap = L.ovf_cap;
+  void* w = const_cast<void*>(ws);
+  a->tile_count = at<int64_t>(w, L.tile_count);
+  a->tile_base = at<int64_t>(w, L.tile_base);
+  a->tile_ovf = at<int64_t>(w, L.tile_ovf);
+  a->region = at<uint64_t>(w, L.region);
+  a->ovf_area = at<uint64_t>(w, L.ovf_area);
+  a->seg_tbase = at<int64_t>(w, L.seg_tbase);
+  a->bad = b->bad_pixel;
+}
+
 evs_status evs_step_voxel(const evs_step_params* p, const evs_step_buffers* b, const void* ws, size_t ws_bytes,
                           int32_t stream_index, int64_t t0, int64_t t1, int32_t bins, int32_t flags, float* out,
                           void* voxel_ws, size_t voxel_ws_bytes, void* stream) {
@@ -417,21 +432,25 @@ evs_status evs_step_voxel(const evs_step_params* p, const evs_step_buffers* b, c
   const bool fin = (flags & EVS_VOXEL_FINALIZE) != 0;
   if (fin ? !out : (!voxel_ws || voxel_ws_bytes < (size_t)bins * P * sizeof(long long))) return EVS_ERR_ARG;
   StepVoxArgs a;
-  memset(&a, 0, sizeof(a));
-  a.ntiles = L.ntiles; a.T = p->frames; a.s = stream_index; a.B = bins; a.W = p->width;
-  a.P = P; a.cap = p->capacity; a.ovf_cap = L.ovf_cap;
-  void* w = const_cast<void*>(ws);
-  a.tile_count = at<int64_t>(w, L.tile_count);
-  a.tile_base = at<int64_t>(w, L.tile_base);
-  a.tile_ovf = at<int64_t>(w, L.tile_ovf);
-  a.region = at<uint64_t>(w, L.region);
-  a.ovf_area = at<uint64_t>(w, L.ovf_area);
-  a.seg_tbase = at<int64_t>(w, L.seg_tbase);
-  a.bad = b->bad_pixel;
+  step_regions(p, b, L, ws, &a);
+  a.s = stream_index; a.B = bins;
   a.t0 = t0; a.t1 = t1;
   a.out = fin ? out : nullptr;
   a.acc_out = fin ? nullptr : static_cast<long long*>(voxel_ws);
   return launch_step_voxel(a, static_cast<cudaStream_t>(stream)) == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
+}
+
+evs_status evs_step_histogram(const evs_step_params* p, const evs_step_buffers* b, const void* ws,
+                              size_t ws_bytes, int64_t window_us, int64_t t_end, int64_t* out, void* stream) {
+  StepLayout L;
+  if (!step_layout(p, &L) || !b || !b->bad_pixel || !out) return EVS_ERR_ARG;
+  if (!ws || ws_bytes < L.total) return EVS_ERR_WORKSPACE;
+  if (p->streams > 65535) return EVS_ERR_ARG;
+  if (L.fast) return EVS_ERR_UNSUPPORTED;
+  StepVoxArgs a;
+  step_regions(p, b, L, ws, &a);
+  return launch_step_hist(a, p->streams, t_end - window_us, t_end, out, static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
 }
 
 evs_status evs_step_clock_init(const evs_step_params* p, void* ws, size_t ws_bytes, int64_t t0,

@@ -232,6 +232,42 @@ cudaError_t launch_step_voxel(const StepVoxArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ---- event histograms of every stream from a step's tile regions ------------
+// accumulate_events_to_image (model.py:249-262) of each stream's events of the
+// step with t in [lo, hi): grid (tile, stream), the tile's pixels summed in
+// shared memory (|sum| <= events of the pixel: int32 is exact), int64 out.
+__global__ void __launch_bounds__(256) k_step_hist(StepVoxArgs a, int64_t lo, int64_t hi, int64_t* out) {
+  __shared__ int acc[kGenTile];
+  const int q = blockIdx.x, s = blockIdx.y, tid = threadIdx.x;
+  for (int i = tid; i < kGenTile; i += blockDim.x) acc[i] = 0;
+  __syncthreads();
+  const int64_t tile0 = (int64_t)q * kGenTile;
+  if (*a.bad == kNoBad) {
+    StepVoxArgs b = a;
+    b.s = s;
+    for (int f = 0; f < a.T; ++f) {
+      const VoxTileSrc r = vox_tile_src(b, q, f);
+      for (int64_t i = tid; i < r.nkeep; i += blockDim.x) {
+        const uint64_t k = __ldcs(r.src + i);
+        const int64_t t = r.tb + (int64_t)(k >> kKeyPixBits);
+        if (t < lo || t >= hi) continue;  // model.py:259
+        const int lp = (int)((int64_t)((k >> 17) & 0xffffu) * a.W + (int64_t)((k >> 1) & 0xffffu) - tile0);
+        atomicAdd(acc + lp, (k & 1u) ? 1 : -1);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < kGenTile; i += blockDim.x) {
+    const int64_t pix = tile0 + i;
+    if (pix < a.P) out[(int64_t)s * a.P + pix] = acc[i];
+  }
+}
+
+cudaError_t launch_step_hist(const StepVoxArgs& a, int S, int64_t lo, int64_t hi, int64_t* out, cudaStream_t st) {
+  k_step_hist<<<dim3(a.ntiles, S), 256, 0, st>>>(a, lo, hi, out);
+  return cudaGetLastError();
+}
+
 // ---- limit_bandwidth -------------------------------------------------------
 // keep[i] = rank of i in its window < cap; per-block kept counts; unsorted flag
 __global__ void __launch_bounds__(1024) k_lb_flags(int64_t n, const int64_t* __restrict__ t, int64_t window,

@@ -404,6 +404,35 @@ class EventSimulator:
         vox(0, None, 1, 0, None, None, None, None, _lib.EVS_VOXEL_FINALIZE)
         return out
 
+    def histograms(self, window_us: int, t_end: int | None = None):
+        """accumulate_events_to_image (model.py:249-262) of every stream's events
+        of the last step with t in [t_end - window_us, t_end) (default t_end: the
+        end of the step): int64 [S, H, W] on the device, one launch for all
+        streams (evs_step_histogram; the bucket path sums the output rows)."""
+        import ctypes
+
+        import torch
+
+        e = self.engine
+        assert e is not None, "call reset() first"
+        if window_us <= 0:
+            raise ValueError("window_us must be positive")
+        t_end = self.t_next if t_end is None else int(t_end)
+        out = torch.empty((self.S, self.H, self.W), dtype=torch.int64, device=self.device)
+        L = _lib.load()
+        rc = L.evs_step_histogram(ctypes.byref(e.params), ctypes.byref(e.bufs), e.workspace.data_ptr(),
+                                  e.workspace.numel(), int(window_us), t_end, out.data_ptr(), _lib.stream_ptr())
+        if rc == _lib.EVS_ERR_UNSUPPORTED:
+            from .represent import accumulate
+            from .events.types import concat_batches
+
+            for s in range(self.S):
+                b = concat_batches([self.segment(s, f) for f in range(self.T)])
+                out[s] = accumulate(b, int(window_us), t_end, self.W, self.H, device_output=True)
+            return out
+        _lib.check(rc, "evs_step_histogram")
+        return out
+
     def voxel(self, batch: DeviceEventBatch, t0: int, t1: int, bins: int = 5):
         from .represent import voxel_grid
 

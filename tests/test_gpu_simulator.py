@@ -214,3 +214,31 @@ def test_voxel_window_wide_window_64bit_bins():
     parts = [oracle.generate(ost, frames[0, f], f * tick, (f + 1) * tick) for f in range(T)]
     exp = oracle.voxel(oracle.concat(parts), 0, T * tick, 5, W, H)
     np.testing.assert_array_equal(sim.voxel_window(0, bins=5).cpu().numpy(), exp)
+
+
+@pytest.mark.parametrize("path", ["tile", "bucket"])
+def test_histograms_all_streams_match_oracle(path, monkeypatch):
+    """EventSimulator.histograms: accumulate_events_to_image of every stream in
+    one launch, windows inside and across the step's frames."""
+    import torch
+
+    from paper_2602_15018_b200.simulator import EventSimulator
+
+    if path == "bucket":
+        monkeypatch.setenv("EVS_PATH", "bucket")
+    S, T, W, H = 5, 3, 346, 260
+    cfg = ev.EventCameraConfig(c_pos=0.2, c_neg=0.2, refractory_us=0)
+    sim = EventSimulator(W, H, streams=S, frames_per_step=T, config=cfg)
+    f0 = [texture_frame(W, H, 0.137 * s) for s in range(S)]
+    sim.reset(f0, seeds=list(range(S)))
+    ost = [oracle.init_state(f0[s], seed=s) for s in range(S)]
+    frames = np.stack([[texture_frame(W, H, 0.137 * s + 0.02 * (f + 1)) for f in range(T)] for s in range(S)])
+    sim.step(torch.from_numpy(frames).cuda())
+    batches = [oracle.concat([oracle.generate(ost[s], frames[s, f], f * 1000, (f + 1) * 1000)
+                              for f in range(T)]) for s in range(S)]
+    for window, t_end in ((2000, 3000), (1500, 2200), (10, 1), (5000, 3000)):
+        got = sim.histograms(window, t_end).cpu().numpy()
+        for s in range(S):
+            assert np.array_equal(got[s], oracle.accumulate(batches[s], window, t_end, W, H)), (window, t_end, s)
+    assert np.array_equal(sim.histograms(1000).cpu().numpy()[2],
+                          oracle.accumulate(batches[2], 1000, 3000, W, H))
