@@ -191,7 +191,7 @@ def main():
                     "with_noise_and_voxel": {"ms_per_window_wall": wall * 1e3, "frames_per_s": T / wall,
                                              "note": "EventSimulator.voxel_window: step + exact 10 Hz noise per "
                                                      "frame + one 5-bin voxel grid per 20-frame window "
-                                                     "(segmented accumulation, one host read per window)",
+                                                     "(signal voxel from the tile regions, noise added by a segmented accumulation, one host read per window)",
                                              "voxel_sum": float(vox.sum().item())},
                     "with_merged_event_batches": {"ms_per_window_wall": wall2 * 1e3, "frames_per_s": T / wall2,
                                                   "note": "per frame: noise, canonical sort, merge-path into the "
