@@ -36,8 +36,54 @@ def unpack_keys(k: torch.Tensor, t_base: int):
     return t, x, y, p
 
 
+def key32_layout(width: int, height: int, span_us: int):
+    """Bit widths (t_rel, y, x) of a 4-byte key t_rel << (yb + xb + 1) | y << (xb + 1)
+    | x << 1 | p for a sensor and a time span (DAVIS events in
+    4 bytes), or None when they need more than 31 bits (the key stays a
+    non-negative int32, so its order is the canonical order)."""
+    def bits(n):
+        return max(1, int(n - 1).bit_length())
+    tb, yb, xb = bits(span_us), bits(height), bits(width)
+    return (tb, yb, xb) if tb + yb + xb + 1 <= 31 else None
+
+
+def pack_keys32(t: torch.Tensor, x: torch.Tensor, y: torch.Tensor, p: torch.Tensor, t_base: int,
+                layout) -> torch.Tensor:
+    """SoA events -> int32 keys (layout from key32_layout; 0 <= t - t_base < 2**tb)."""
+    tb, yb, xb = layout
+    tr = (t - t_base).to(torch.int64)
+    k = (tr << (yb + xb + 1)) | ((y.to(torch.int64) & 0xFFFF) << (xb + 1)) | \
+        ((x.to(torch.int64) & 0xFFFF) << 1) | (p > 0).to(torch.int64)
+    return k.to(torch.int32)
+
+
+def unpack_keys32(k: torch.Tensor, t_base: int, layout):
+    tb, yb, xb = layout
+    k = k.to(torch.int64)
+    t = (k >> (yb + xb + 1)) + t_base
+    y = ((k >> (xb + 1)) & ((1 << yb) - 1)).to(torch.int32)
+    x = ((k >> 1) & ((1 << xb) - 1)).to(torch.int32)
+    p = torch.where((k & 1) == 1, 1, -1).to(torch.int8)
+    return t, x, y, p
+
+
+def gather_events(t, x, y, p, t_base: int, width: int, height: int, span_us: int, dst: int = 0, group=None):
+    """Gather every rank's events (SoA, times in [t_base, t_base + span_us)) to
+    ``dst`` in rank order as packed keys: 4 bytes per event when the sensor and
+    span fit in 31 bits (DAVIS: 12 + 9 + 9 + 1), else 8.  Returns (t, x, y, p)
+    on dst, None elsewhere; the same layout decision on every rank."""
+    lay = key32_layout(width, height, span_us)
+    if lay is None:
+        keys = pack_keys(t, x, y, p, t_base)
+        out, _ = gather_keys(keys, dst=dst, group=group)
+        return None if out is None else unpack_keys(out, t_base)
+    keys = pack_keys32(t, x, y, p, t_base, lay)
+    out, _ = gather_keys(keys, dst=dst, group=group)
+    return None if out is None else unpack_keys32(out, t_base, lay)
+
+
 def gather_keys(local: torch.Tensor, dst: int = 0, group=None):
-    """Gatherv of 1-D int64 tensors to `dst`.  Returns (concatenated, counts) on
+    """Gatherv of 1-D int64 / int32 tensors to `dst`.  Returns (concatenated, counts) on
     dst and (None, counts) elsewhere.  Rank order is preserved."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)

@@ -9,7 +9,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2602_15018_b200.distributed import gather_fixed, gather_keys, pack_keys, shard_streams, unpack_keys
+from paper_2602_15018_b200.distributed import (gather_events, gather_fixed, gather_keys, key32_layout, pack_keys,
+                                               pack_keys32, shard_streams, unpack_keys, unpack_keys32)
 
 
 def _free_port():
@@ -33,8 +34,22 @@ def _worker(rank, world, port, q):
         out, counts = gather_keys(keys, dst=0)
         hist = torch.full((3, 4), rank, dtype=torch.int64)
         stacked = gather_fixed(hist, dst=0)
+        # DAVIS-sized events travel as 4-byte keys, HD ones with a long span as 8-byte keys
+        ev = []
+        for W, H, span in ((346, 260, 4000), (1280, 720, 1 << 20)):
+            n = 50 + 30 * rank
+            g = torch.Generator().manual_seed(rank)
+            tt = torch.randint(0, span, (n,), generator=g) + 7000
+            xx = torch.randint(0, W, (n,), generator=g).to(torch.int16)
+            yy = torch.randint(0, H, (n,), generator=g).to(torch.int16)
+            pp = (torch.randint(0, 2, (n,), generator=g) * 2 - 1).to(torch.int8)
+            got = gather_events(tt, xx, yy, pp, 7000, W, H, span, dst=0)
+            ev.append((tt.tolist(), xx.tolist(), yy.tolist(), pp.tolist(),
+                       None if got is None else [v.tolist() for v in got]))
         if rank == 0:
-            q.put(("ok", counts, out.tolist(), stacked.tolist()))
+            q.put(("ok", counts, out.tolist(), stacked.tolist(), ev))
+        else:
+            q.put(("r1", ev))
     finally:
         dist.destroy_process_group()
 
@@ -67,11 +82,15 @@ def test_gatherv_two_ranks_gloo():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for pr in procs:
         pr.start()
-    res = q.get(timeout=100)
+    got = dict((r[0], r) for r in (q.get(timeout=100), q.get(timeout=100)))
     for pr in procs:
         pr.join(timeout=60)
-    assert res[0] == "ok"
+    res, r1 = got["ok"], got["r1"]
     counts, out, stacked = res[1], res[2], res[3]
+    for (t0, x0, y0, p0, merged), (t1, x1, y1, p1, _none) in zip(res[4], r1[1]):
+        t, x, y, p = merged
+        assert t == t0 + t1 and p == p0 + p1
+        assert x == [v & 0xFFFF for v in x0 + x1] and y == [v & 0xFFFF for v in y0 + y1]
     assert counts == [4 * 1, 4 * 4]
     keys = torch.tensor(out)
     t, x, y, p = unpack_keys(keys, 1000)
@@ -79,3 +98,22 @@ def test_gatherv_two_ranks_gloo():
     assert x[:4].tolist() == [1] * 4 and x[4:].tolist() == [2] * 16
     assert t[:4].tolist() == [1000, 1001, 1002, 1003]
     assert stacked[0][0][0] == 0 and stacked[1][2][3] == 1
+
+
+def test_key32_layout_roundtrip_and_order():
+    assert key32_layout(346, 260, 4000) == (12, 9, 9)
+    assert key32_layout(1280, 720, 50_000) is None
+    lay = key32_layout(640, 480, 2000)
+    g = torch.Generator().manual_seed(3)
+    n = 5000
+    t = torch.randint(0, 2000, (n,), generator=g) + 10**9
+    x = torch.randint(0, 640, (n,), generator=g).to(torch.int16)
+    y = torch.randint(0, 480, (n,), generator=g).to(torch.int16)
+    p = (torch.randint(0, 2, (n,), generator=g) * 2 - 1).to(torch.int8)
+    k = pack_keys32(t, x, y, p, 10**9, lay)
+    assert k.dtype == torch.int32 and int(k.min()) >= 0
+    t2, x2, y2, p2 = unpack_keys32(k, 10**9, lay)
+    assert torch.equal(t2, t) and torch.equal(x2, x.to(torch.int32)) and torch.equal(y2, y.to(torch.int32))
+    assert torch.equal(p2, p)
+    # int32 key order == the 8-byte key order == canonical (t, y, x, p)
+    assert torch.equal(torch.argsort(k, stable=True), torch.argsort(pack_keys(t, x, y, p, 10**9), stable=True))
