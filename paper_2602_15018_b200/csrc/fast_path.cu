@@ -81,6 +81,7 @@ __device__ __noinline__ double fast_log_g(double x) {
 // (model.py:125-137); returns n (0: no crossing) and |diff|, th.
 __device__ __noinline__ int exact_count(float v, float r, float thp, float thn, double log_eps, bool& pos,
                                         double& ad, double& thd) {
+  if (!(v >= 0.f && v <= 1.f)) return 0;  // invalid intensity: the call is rejected by validation
   const double ln = fast_log_g((double)v + log_eps);  // model.py:39
   const double diff = ln - (double)r;
   pos = diff > 0.0;
@@ -89,7 +90,7 @@ __device__ __noinline__ int exact_count(float v, float r, float thp, float thn, 
   ad = pos ? diff : -diff;
   const double q = __dadd_rn(__ddiv_rn(ad, thd), 1e-4);  // int(|diff|/th + 1e-4)
   if (!(q >= 1.0)) return 0;
-  return q > 2147483647.0 ? 2147483647 : (int)q;
+  return q > (double)kMaxPixelCrossings ? 0 : (int)q;  // (beyond: corrupt level, no 32-bit overflow)
 }
 // t_rel of crossing j (model.py:144-146)
 __device__ __forceinline__ int exact_trel(int j, double thd, double ad, double dtd, int dtm1) {

@@ -7,6 +7,10 @@ namespace evs {
 
 constexpr int64_t kNoBad = 0x7fffffffffffffffLL;
 constexpr int kHistReps = 8;      // replicated global histograms (atomic spread)
+// crossings of one pixel in one frame: <= (ln(1 + eps) - ln(eps)) / 0.01 + 1 for
+// a reference level inside the log range (462 at eps = 0.01, MIN_THRESHOLD);
+// more only comes from a corrupt level and fails the call (no 32-bit overflow)
+constexpr int64_t kMaxPixelCrossings = 1 << 20;
 constexpr int kMaxDigitBits = 11; // onesweep digit width (<= 2048 bins)
 constexpr int kKeyPixBits = 33;   // key = t_rel << 33 | y << 17 | x << 1 | (p > 0)
 
@@ -71,7 +75,7 @@ struct GenArgs {
   uint64_t* ovf_area;        // [nseg][ovf_cap]
   unsigned long long* ovf_cursor;  // [nseg], zeroed by the prologue
   int64_t ovf_cap;
-  int64_t* err;              // [1] != 0: overflow area exhausted
+  int64_t* err;              // [1] bit 0: overflow area exhausted, bit 1: corrupt level (> kMaxPixelCrossings)
   int gt;                    // tiles per group (histogram row)
   // frame chunking: block b handles chunk c = b / (S*ntiles) = frames
   // [c*tc, min(T, (c+1)*tc)) of its tile; chunk c waits for chunk c-1 of the
@@ -105,7 +109,7 @@ struct TileScanArgs {
   int64_t* out_count;
   int64_t* out_dropped;
   const int64_t* bad;
-  const int64_t* err;         // K1 overflow-area exhaustion -> out_dropped = -1
+  const int64_t* err;         // K1 errors -> out_dropped = -1 (overflow area) / -2 (corrupt level)
   int gt;
   // fused validation: restore the state from the backup when a frame was invalid
   const float* bak_ref;

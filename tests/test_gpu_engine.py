@@ -132,3 +132,40 @@ def test_invalid_frame_leaves_state_untouched(T):
     assert bad == (1 * T + 1) * H * W + 3 * W + 5
     assert torch.equal(ref, ref0) and torch.equal(last, last0)
     assert int(counts.sum()) == 0
+
+
+@pytest.mark.parametrize("bucket", [False, True])
+def test_infinite_intensity_rejected_fast_and_state_kept(bucket, monkeypatch):
+    """+inf / huge values: the call is rejected (first bad pixel) without
+    running the crossing loops on them (an inf once meant ~2^31 crossings)."""
+    import time
+
+    import torch
+
+    if bucket:
+        monkeypatch.setenv("EVS_PATH", "bucket")
+    H, W = 40, 160
+    for T in (1, 5):
+        frames, ost, ref, last, thp, thn, eng = _setup(1, T, H, W, (0.1, 0.1), [0])
+        frames[0, 0, 20, 9] = np.inf
+        frames[0, T - 1, 3, 4] = 1e30
+        ref0, last0 = ref.clone(), last.clone()
+        t0 = time.time()
+        eng.launch(torch.from_numpy(frames).cuda(), ref, last, t0=0, tick=1000)
+        counts, dropped, res, bad = eng.fetch_info()
+        assert time.time() - t0 < 5.0
+        assert bad == (3 * W + 4 if T == 1 else 20 * W + 9)
+        assert torch.equal(ref, ref0) and torch.equal(last, last0)
+
+
+def test_corrupt_reference_level_fails_loudly():
+    import torch
+
+    from paper_2602_15018_b200._lib import NativeError
+
+    H, W = 16, 64
+    frames, ost, ref, last, thp, thn, eng = _setup(1, 1, H, W, (0.1, 0.1), [0])
+    ref[0, 5, 7] = -1e30  # |diff| / th ~ 1e31 crossings
+    eng.launch(torch.from_numpy(frames).cuda(), ref, last, t0=0, tick=1000)
+    with pytest.raises(NativeError, match="2\\*\\*20"):
+        eng.fetch_info()
