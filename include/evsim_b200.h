@@ -92,7 +92,8 @@ typedef struct evs_step_buffers {
   int64_t* counts;         /* [S*T] events written (= min(kept, capacity)) */
   int64_t* dropped;        /* [S*T] EventBatch.dropped_count; -1: the tile-overflow area was
                               exhausted, -2: a pixel would cross > 2^20 thresholds in one frame
-                              (corrupt ref_log) -- the call's outputs are then invalid */
+                              (+inf intensity without validation, or a corrupt ref_log)
+                              -- the call's outputs are then invalid */
   int64_t* reservations;   /* [S*T] AggregationStats.reservation_count */
   int64_t* bad_pixel;      /* [1] must hold INT64_MAX on entry; receives the first
                               invalid flat index into frames (s*T*H*W + f*H*W + i) */

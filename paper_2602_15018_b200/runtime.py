@@ -179,8 +179,9 @@ class StepEngine:
         host = torch.cat([self.info.reshape(-1), self.bad]).cpu().numpy()
         nseg = self.info.shape[1]
         if int(host[-1]) == _lib.NO_BAD and (host[nseg:2 * nseg] == -2).any():
-            raise _lib.NativeError("a pixel would cross more than 2**20 thresholds in one frame: the reference "
-                                   "level (ref_log) lies far outside the log range of [0, 1] intensities")
+            raise _lib.NativeError("a pixel would cross more than 2**20 thresholds in one frame: an infinite "
+                                   "intensity (with validate=False) or a reference level (ref_log) far outside "
+                                   "the log range of [0, 1] intensities")
         if int(host[-1]) == _lib.NO_BAD and (host[nseg:2 * nseg] < 0).any():
             raise _lib.NativeError("event overflow area exhausted (a frame far above its capacity "
                                    "concentrated > 4 events/pixel in many tiles); raise max_events_per_frame")
