@@ -19,6 +19,7 @@
  *   evs_voxel_segments  the same over many device-counted segments (a window)
  *   evs_step_voxel      the same from a step's per-tile regions (no atomics)
  *   evs_step_histogram  accumulate_events_to_image of every stream of a step
+ *   evs_compact_segments packs a step's segments back to back (one D2H per array)
  *   evs_limit_bandwidth limit_bandwidth           evsim/events/model.py:215-246
  *   evs_render          render_pair               evsim/render.py:179-208 (frame producer)
  *   evs_seed_pcg64      numpy default_rng(seed) seeding used by
@@ -216,6 +217,15 @@ evs_status evs_step_voxel(const evs_step_params* p, const evs_step_buffers* b, c
 evs_status evs_step_histogram(const evs_step_params* p, const evs_step_buffers* b, const void* workspace,
                               size_t workspace_bytes, int64_t window_us, int64_t t_end, int64_t* out,
                               void* stream);
+
+/* Pack the first counts[g] (device int64) events of every segment g < nseg of
+ * an evs_step output (stride seg_stride = capacity) back to back into out_*
+ * (segment order), so a host copy is one transfer per array.  Nothing is
+ * written at or beyond out_capacity elements (the caller compares the total). */
+evs_status evs_compact_segments(int32_t nseg, const int64_t* counts, int64_t seg_stride, const int64_t* t,
+                                const uint16_t* x, const uint16_t* y, const int8_t* p, int64_t* out_t,
+                                uint16_t* out_x, uint16_t* out_y, int8_t* out_p, int64_t out_capacity,
+                                void* stream);
 
 /* limit_bandwidth (model.py:215-246) of a t-sorted device batch of n >= 1
  * events: keeps the first `cap` = int(rate * window * 1e-6) events of each

@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "evs_version", "evs_error_string", "evs_step_workspace_bytes", "evs_step",
     "evs_step_profiled", "evs_step_clock_init",
     "evs_sort_workspace_bytes", "evs_canonical_sort", "evs_batch_stats", "evs_seed_pcg64",
-    "evs_noise_workspace_bytes", "evs_noise", "evs_accumulate", "evs_voxel", "evs_voxel_segments", "evs_step_voxel", "evs_step_histogram",
+    "evs_noise_workspace_bytes", "evs_noise", "evs_accumulate", "evs_voxel", "evs_voxel_segments", "evs_step_voxel", "evs_step_histogram", "evs_compact_segments",
     "evs_limit_bandwidth_workspace_bytes", "evs_limit_bandwidth", "evs_render",
 )
 
@@ -147,6 +147,7 @@ def _bind_extras(L) -> None:
     L.evs_voxel_segments.argtypes = [i32, P, i64, i64, P, P, P, P, i64, i64, i32, i32, i32, i32, P, P, sz, P]
     L.evs_step_voxel.argtypes = [P, P, P, sz, i32, i64, i64, i32, i32, P, P, sz, P]
     L.evs_step_histogram.argtypes = [P, P, P, sz, i64, i64, P, P]
+    L.evs_compact_segments.argtypes = [i32, P, i64, P, P, P, P, P, P, P, P, i64, P]
     L.evs_limit_bandwidth_workspace_bytes.restype = sz
     L.evs_limit_bandwidth_workspace_bytes.argtypes = [i64]
     L.evs_limit_bandwidth.argtypes = [i64, P, P, P, P, i64, i64, P, P, P, P, P, P, sz, P]

@@ -268,6 +268,32 @@ cudaError_t launch_step_hist(const StepVoxArgs& a, int S, int64_t lo, int64_t hi
   return cudaGetLastError();
 }
 
+// ---- segment compaction -----------------------------------------------------
+// out[prefix_g + i] = in[g * seg_stride + i] for i < counts[g], all four SoA
+// arrays; prefix_g = sum of the earlier counts (each CTA sums them itself).
+__global__ void __launch_bounds__(256) k_compact_segments(const int64_t* __restrict__ counts, int64_t seg_stride,
+                                                          const int64_t* __restrict__ t, const uint16_t* __restrict__ x,
+                                                          const uint16_t* __restrict__ y, const int8_t* __restrict__ p,
+                                                          int64_t* ot, uint16_t* ox, uint16_t* oy, int8_t* op,
+                                                          int64_t out_cap) {
+  __shared__ int64_t s_pre[9];
+  const int g = blockIdx.y, tid = threadIdx.x;
+  int64_t part = 0;
+  for (int j = tid; j < g; j += blockDim.x) part += counts[j];
+  int64_t tot;
+  block_excl_scan<256, int64_t>(part, s_pre, &tot);
+  const int64_t pre = tot;
+  int64_t n = counts[g];
+  if (pre + n > out_cap) n = out_cap - pre;  // (caller falls back when the total exceeds out_cap)
+  const int64_t src = (int64_t)g * seg_stride;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + tid; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    ot[pre + i] = __ldcs(t + src + i);
+    ox[pre + i] = __ldcs(x + src + i);
+    oy[pre + i] = __ldcs(y + src + i);
+    op[pre + i] = __ldcs(p + src + i);
+  }
+}
+
 // ---- limit_bandwidth -------------------------------------------------------
 // keep[i] = rank of i in its window < cap; per-block kept counts; unsorted flag
 __global__ void __launch_bounds__(1024) k_lb_flags(int64_t n, const int64_t* __restrict__ t, int64_t window,
@@ -391,6 +417,19 @@ evs_status evs_voxel_segments(int32_t nseg, const int64_t* counts, int64_t count
   }
   if (flags & EVS_VOXEL_FINALIZE)
     k_voxel_finalize<<<grid_for((int64_t)bins * P, 148 * 16), 256, 0, st>>>((int64_t)bins * P, acc, t1 - t0, out);
+  return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
+}
+
+evs_status evs_compact_segments(int32_t nseg, const int64_t* counts, int64_t seg_stride, const int64_t* t,
+                                const uint16_t* x, const uint16_t* y, const int8_t* p, int64_t* out_t,
+                                uint16_t* out_x, uint16_t* out_y, int8_t* out_p, int64_t out_capacity,
+                                void* stream) {
+  if (nseg < 0 || nseg > 65535 || seg_stride < 0 || out_capacity < 0) return EVS_ERR_ARG;
+  if (nseg == 0) return EVS_OK;
+  if (!counts || !t || !x || !y || !p || !out_t || !out_x || !out_y || !out_p) return EVS_ERR_ARG;
+  const int bx = (148 * 8 + nseg - 1) / nseg;
+  k_compact_segments<<<dim3(bx < 2 ? 2 : bx, nseg), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      counts, seg_stride, t, x, y, p, out_t, out_x, out_y, out_p, out_capacity);
   return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
 }
 

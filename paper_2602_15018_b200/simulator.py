@@ -176,7 +176,7 @@ class EventSimulator:
         import torch
 
         from .events.types import EventBatch
-        from .runtime import PinnedPool, StepEngine, d2h_segments
+        from .runtime import PinnedPool, StepEngine, compact_launch, d2h_packed
 
         assert self.engine is not None, "call reset() first"
         dev = self.device
@@ -192,6 +192,7 @@ class EventSimulator:
         ev_h2d = [torch.cuda.Event() for _ in range(2)]
         ev_comp = [torch.cuda.Event() for _ in range(2)]
         ev_d2h = [torch.cuda.Event() for _ in range(2)]
+        scratch = [{}, {}]  # device staging of the packed segments, one per pool
         for e in ev_comp + ev_d2h:
             e.record(comp)
 
@@ -217,6 +218,9 @@ class EventSimulator:
             comp.wait_event(ev_d2h[i % 2])  # window i-2's results have left this pool
             eng.launch(fbuf[i % 2], self.ref, self.last, self.thp, self.thn, t0=self.t_next, tick=self.tick,
                        validate=validate, stream=comp)
+            rows = [eng.ev_t, eng.ev_x, eng.ev_y, eng.ev_p]
+            with torch.cuda.stream(comp):  # pack the segments behind the step (copy engine stays busy)
+                packed = compact_launch(eng.info[0], rows, scratch[i % 2])
             ev_comp[i % 2].record(comp)
             self.t_next += self.T * self.tick
             self.step_index += 1
@@ -229,8 +233,7 @@ class EventSimulator:
                 raise ValueError(f"invalid intensity in window {i} (flat index {int(bad)})")
             with torch.cuda.stream(d2h):
                 d2h.wait_event(ev_comp[i % 2])
-                t, x, y, p = d2h_segments(self._pool, counts, [eng.ev_t, eng.ev_x, eng.ev_y, eng.ev_p],
-                                          sync=False)
+                t, x, y, p = d2h_packed(self._pool, counts, rows, scratch[i % 2], packed, sync=False)
                 ev_d2h[i % 2].record(d2h)
             dr = dropped.reshape(self.S, self.T)
             batches = [[EventBatch(t=t[g].view(np.uint64), x=x[g].view(np.uint16), y=y[g].view(np.uint16),
