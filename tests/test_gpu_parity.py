@@ -67,6 +67,15 @@ def test_capacity_overflow_large_frame():
     _sequence(640, 480, 3, cfg, seed=2)
 
 
+@pytest.mark.parametrize("W,H,api", [(65535, 3, "parallel"), (3, 65535, "parallel"), (65535, 2, "serial"),
+                                      (1, 1, "parallel"), (31, 1, "serial")])
+def test_extreme_shapes(W, H, api):
+    """Coordinates at the 16-bit limits of the packed keys (x or y = 65534),
+    one-pixel and one-row sensors."""
+    _sequence(W, H, 3, ev.EventCameraConfig(c_pos=0.1, c_neg=0.1, refractory_us=50), seed=3, api=api,
+              drift=0.07)
+
+
 def test_noise_golden():
     g = dict(np.load(os.path.join(GOLD, "noise.npz")))
     i = 0
