@@ -236,10 +236,6 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
              ((uintptr_t)b->last_event_t % 16 == 0) &&
              (b->th_pos == nullptr || (((uintptr_t)b->th_pos % 16 == 0) && ((uintptr_t)b->th_neg % 16 == 0)));
     fa.log_eps = p->log_eps; fa.log_eps_f = (float)p->log_eps;
-    {
-      const char* dbg = getenv("EVS_FAST_DBG");
-      fa.dbg = dbg ? atoi(dbg) : 0;
-    }
     fa.refr = (int)p->refractory_us;
     fa.thp_u = p->th_pos_uniform; fa.thn_u = p->th_neg_uniform;
     fa.rthp_u = (float)(1.0 / (double)p->th_pos_uniform);

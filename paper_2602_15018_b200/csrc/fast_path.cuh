@@ -34,7 +34,6 @@ constexpr int64_t kSrcSlot = -1, kSrcRedo = -3;
 
 struct FastArgs {
   int S, T, W, G, ntiles, nbk, vec;
-  int dbg;  // timing experiments only (EVS_FAST_DBG): 1 = K1 math only
   int64_t P;
   double log_eps;
   float log_eps_f;
