@@ -139,18 +139,22 @@ class EventSimulator:
         import torch
 
         from .events.types import EventBatch
-        from .runtime import PinnedPool, d2h_segments
+        from .runtime import PinnedPool, compact_launch, d2h_packed
 
         fr = np.ascontiguousarray(frames_host, np.float32)
         if fr.ndim == 3:
             fr = fr[:, None]
         dfr = torch.from_numpy(fr).to(self.device)
         self.step(dfr, validate=validate)
-        res = self.result()
+        e = self.engine
+        rows = [e.ev_t, e.ev_x, e.ev_y, e.ev_p]
         if not hasattr(self, "_pool"):
             self._pool = PinnedPool()
-        e = self.engine
-        t, x, y, p = d2h_segments(self._pool, res.counts.ravel(), [e.ev_t, e.ev_x, e.ev_y, e.ev_p])
+        if not hasattr(self, "_step_scratch"):
+            self._step_scratch = {}
+        packed = compact_launch(e.info[0], rows, self._step_scratch)  # behind the step, before the host read
+        res = self.result()
+        t, x, y, p = d2h_packed(self._pool, res.counts.ravel(), rows, self._step_scratch, packed)
         out = []
         for s in range(self.S):
             row = []
