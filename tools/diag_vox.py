@@ -45,3 +45,4 @@ print("step            ms (device, wall)", timed(lambda: sim.step(fr[:, :T])))
 print("voxel signal    ms", timed(lambda: sim.voxel_window(0, bins=5)))
 print("voxel +noise    ms", timed(lambda: sim.voxel_window(0, bins=5, noise_seeds=seeds())))
 print("step+vox+noise  ms", timed(lambda: (sim.step(fr[:, :T]), sim.voxel_window(0, bins=5, noise_seeds=seeds()))))
+print("histograms ms", timed(lambda: sim.histograms(20 * 1000)))
