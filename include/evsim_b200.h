@@ -14,6 +14,7 @@
  *                        and log_transform validation, model.py:28-39)
  *   evs_canonical_sort  canonical_sort            evsim/events/parallel.py:112-123
  *   evs_noise           inject_noise_events       evsim/events/model.py:174-212
+ *   evs_noise_batch     the same for the frames of a window, batched launches
  *   evs_accumulate      accumulate_events_to_image evsim/events/model.py:249-262
  *   evs_voxel           (no reference counterpart; repo-defined voxel grid)
  *   evs_voxel_segments  the same over many device-counted segments (a window)
@@ -165,6 +166,16 @@ int64_t evs_noise_capacity(const evs_noise_params* p);
 evs_status evs_noise(const evs_noise_params* p, int64_t* ev_t, uint16_t* ev_x, uint16_t* ev_y,
                      int8_t* ev_p, uint64_t* ev_key, int64_t* meta_out, void* workspace,
                      size_t workspace_bytes, void* stream);
+
+/* evs_noise for nf frames at once (e.g. the ticks of one window), batched
+ * kernel launches: frame f's events go to row f (element offset f*ev_stride,
+ * ev_stride >= that frame's evs_noise_capacity; order 0 only) and its meta to
+ * meta_out[4f..4f+3] (same meaning as evs_noise; a flagged frame is redone by
+ * the caller with evs_noise).  Workspace: evs_noise_batch_workspace_bytes. */
+size_t evs_noise_batch_workspace_bytes(const evs_noise_params* ps, int32_t nf);
+evs_status evs_noise_batch(const evs_noise_params* ps, int32_t nf, int64_t* ev_t, uint16_t* ev_x, uint16_t* ev_y,
+                           int8_t* ev_p, int64_t ev_stride, int64_t* meta_out, void* workspace,
+                           size_t workspace_bytes, void* stream);
 
 /* accumulate_events_to_image (model.py:249-262) of a device batch into an
  * int64 (H, W) grid; the caller checks coordinate bounds first (ValueError,

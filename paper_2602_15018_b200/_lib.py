@@ -29,7 +29,9 @@ EXPORTED_SYMBOLS = (
     "evs_version", "evs_error_string", "evs_step_workspace_bytes", "evs_step",
     "evs_step_profiled", "evs_step_clock_init",
     "evs_sort_workspace_bytes", "evs_canonical_sort", "evs_batch_stats", "evs_seed_pcg64",
-    "evs_noise_workspace_bytes", "evs_noise", "evs_accumulate", "evs_voxel", "evs_voxel_segments", "evs_step_voxel", "evs_step_histogram", "evs_compact_segments",
+    "evs_noise_workspace_bytes", "evs_noise", "evs_noise_batch_workspace_bytes", "evs_noise_batch",
+    "evs_accumulate", "evs_voxel", "evs_voxel_segments", "evs_step_voxel", "evs_step_histogram",
+    "evs_compact_segments",
     "evs_limit_bandwidth_workspace_bytes", "evs_limit_bandwidth", "evs_render",
 )
 
@@ -140,6 +142,9 @@ def _bind_extras(L) -> None:
     L.evs_noise_capacity.restype = i64
     L.evs_noise_capacity.argtypes = [ctypes.POINTER(NoiseParams)]
     L.evs_noise.argtypes = [ctypes.POINTER(NoiseParams), P, P, P, P, P, P, P, sz, P]
+    L.evs_noise_batch_workspace_bytes.restype = sz
+    L.evs_noise_batch_workspace_bytes.argtypes = [P, i32]
+    L.evs_noise_batch.argtypes = [P, i32, P, P, P, P, i64, P, P, sz, P]
     L.evs_accumulate.argtypes = [i64, P, P, P, P, i64, i64, i32, i32, P, P]
     L.evs_voxel_workspace_bytes.restype = sz
     L.evs_voxel_workspace_bytes.argtypes = [i32, i32, i32]

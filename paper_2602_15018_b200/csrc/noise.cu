@@ -17,6 +17,7 @@
 // pixel and the stream splits into independent segments at those draws.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -183,8 +184,9 @@ __device__ __forceinline__ void noise_walk_body(const NoiseArgs& a, int64_t c, i
 // (EMIT=true): each walker's exclusive prefix = block prefix (k_noise_scan)
 // + in-block scan, then the labelling walk.
 template <bool EMIT>
-__global__ void __launch_bounds__(256) k_noise_walk(NoiseArgs a) {
+__device__ __forceinline__ void noise_walk(const NoiseArgs& a) {
   __shared__ int64_t s1[9], s2[9];
+  if (blockIdx.x >= a.nblk) return;  // (batched launch: a smaller frame)
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool mine = c < a.nthreads;
   int64_t term = 0, ev = 0;
@@ -212,7 +214,7 @@ __global__ void __launch_bounds__(256) k_noise_walk(NoiseArgs a) {
 // sums its kNsPer consecutive entries, one block scan per array, prefixes
 // written back through shared memory with coalesced stores.
 constexpr int kNsPer = 4, kNsChunk = 1024 * kNsPer;
-__global__ void __launch_bounds__(1024) k_noise_scan(NoiseArgs a) {
+__device__ __forceinline__ void noise_scan(const NoiseArgs& a) {
   extern __shared__ __align__(16) unsigned char nsm[];
   int64_t* sT = reinterpret_cast<int64_t*>(nsm);  // [kNsChunk]
   int64_t* sE = sT + kNsChunk;                    // [kNsChunk]
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(1024) k_noise_scan(NoiseArgs a) {
 }
 
 // per event: timestamp draw D + k and polarity byte k of the u32 stream
-__global__ void __launch_bounds__(256) k_noise_draws(NoiseArgs a) {
+__device__ __forceinline__ void noise_draws(const NoiseArgs& a) {
   const int64_t total = a.meta[1], D = a.meta[0];
   if (a.meta[2] || D < 0) return;
   if (total > a.cap) { if (blockIdx.x == 0 && threadIdx.x == 0) a.meta[3] = 1; return; }
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(256) k_noise_draws(NoiseArgs a) {
 
 // per event: rank within its pixel (reference order: t_rel, then draw order;
 // merge order: polarity, t_rel, draw order) and write the output
-__global__ void __launch_bounds__(256) k_noise_place(NoiseArgs a) {
+__device__ __forceinline__ void noise_place(const NoiseArgs& a) {
   const int64_t total = a.meta[1];
   if (a.meta[2] || a.meta[3] || a.meta[0] < 0) return;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
@@ -328,6 +330,18 @@ __global__ void __launch_bounds__(256) k_noise_place(NoiseArgs a) {
     }
   }
 }
+
+// Up to kNoiseBatch frames per launch (grid.y = frame): each frame's own
+// NoiseArgs; the per-frame walks are short, so batching fills the GPU.
+constexpr int kNoiseBatch = 16;
+struct NoiseBatch {
+  NoiseArgs a[kNoiseBatch];
+};
+template <bool EMIT>
+__global__ void __launch_bounds__(256) k_noise_walk(const __grid_constant__ NoiseBatch b) { noise_walk<EMIT>(b.a[blockIdx.y]); }
+__global__ void __launch_bounds__(1024) k_noise_scan(const __grid_constant__ NoiseBatch b) { noise_scan(b.a[blockIdx.y]); }
+__global__ void __launch_bounds__(256) k_noise_draws(const __grid_constant__ NoiseBatch b) { noise_draws(b.a[blockIdx.y]); }
+__global__ void __launch_bounds__(256) k_noise_place(const __grid_constant__ NoiseBatch b) { noise_place(b.a[blockIdx.y]); }
 
 }  // namespace evs
 
@@ -386,13 +400,8 @@ int64_t evs_noise_capacity(const evs_noise_params* p) {
   return noise_layout(p, &L) ? L.cap : -1;
 }
 
-evs_status evs_noise(const evs_noise_params* p, int64_t* ev_t, uint16_t* ev_x, uint16_t* ev_y, int8_t* ev_p,
-                     uint64_t* ev_key, int64_t* meta_out, void* ws, size_t ws_bytes, void* stream) {
-  NoiseLayout L;
-  if (!noise_layout(p, &L)) return EVS_ERR_ARG;
-  if (!ws || ws_bytes < L.total) return EVS_ERR_WORKSPACE;
-  if (p->order == 1 ? !ev_key : (!ev_t || !ev_x || !ev_y || !ev_p)) return EVS_ERR_ARG;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+static NoiseArgs noise_args(const evs_noise_params* p, const NoiseLayout& L, void* ws, int64_t* ev_t,
+                            uint16_t* ev_x, uint16_t* ev_y, int8_t* ev_p, uint64_t* ev_key, int64_t* meta_out) {
   NoiseArgs a;
   memset(&a, 0, sizeof(a));
   a.P = (int64_t)p->width * p->height;
@@ -424,8 +433,19 @@ evs_status evs_noise(const evs_noise_params* p, int64_t* ev_t, uint16_t* ev_x, u
   a.ev_pol = at<int8_t>(ws, L.ev_pol);
   a.order = p->order;
   a.out_t = ev_t; a.out_x = ev_x; a.out_y = ev_y; a.out_p = ev_p; a.out_key = ev_key;
-  const unsigned gw = (unsigned)((L.nthreads + 255) / 256);
-  k_noise_walk<false><<<gw, 256, 0, st>>>(a);
+  return a;
+}
+
+// the five passes over nf frames of one batch (grid.y = frame)
+static cudaError_t launch_noise(const NoiseBatch& b, const NoiseLayout* Ls, int nf, cudaStream_t st) {
+  int64_t gw = 1, gd = 1, gp = 1;
+  for (int f = 0; f < nf; ++f) {
+    const NoiseLayout& L = Ls[f];
+    gw = std::max<int64_t>(gw, (L.nthreads + 255) / 256);
+    gd = std::max<int64_t>(gd, (L.cap / 16 + 255) / 256 + 1);
+    gp = std::max<int64_t>(gp, L.cap < 148 * 1024 ? (L.cap + 255) / 256 + 1 : 148 * 4);
+  }
+  k_noise_walk<false><<<dim3((unsigned)gw, nf), 256, 0, st>>>(b);
   {
     static bool raised = false;
     const int smem = 2 * kNsChunk * (int)sizeof(int64_t);
@@ -433,14 +453,65 @@ evs_status evs_noise(const evs_noise_params* p, int64_t* ev_t, uint16_t* ev_x, u
       cudaFuncSetAttribute(k_noise_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       raised = true;
     }
-    k_noise_scan<<<1, 1024, smem, st>>>(a);
+    k_noise_scan<<<dim3(1, nf), 1024, smem, st>>>(b);
   }
-  k_noise_walk<true><<<gw, 256, 0, st>>>(a);
-  const unsigned gd = (unsigned)((L.cap / 16 + 255) / 256 + 1);
-  k_noise_draws<<<gd, 256, 0, st>>>(a);
-  const unsigned gp = (unsigned)(L.cap < 148 * 1024 ? (L.cap + 255) / 256 + 1 : 148 * 4);
-  k_noise_place<<<gp, 256, 0, st>>>(a);
-  return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
+  k_noise_walk<true><<<dim3((unsigned)gw, nf), 256, 0, st>>>(b);
+  k_noise_draws<<<dim3((unsigned)gd, nf), 256, 0, st>>>(b);
+  k_noise_place<<<dim3((unsigned)gp, nf), 256, 0, st>>>(b);
+  return cudaGetLastError();
+}
+
+evs_status evs_noise(const evs_noise_params* p, int64_t* ev_t, uint16_t* ev_x, uint16_t* ev_y, int8_t* ev_p,
+                     uint64_t* ev_key, int64_t* meta_out, void* ws, size_t ws_bytes, void* stream) {
+  NoiseLayout L;
+  if (!noise_layout(p, &L)) return EVS_ERR_ARG;
+  if (!ws || ws_bytes < L.total) return EVS_ERR_WORKSPACE;
+  if (p->order == 1 ? !ev_key : (!ev_t || !ev_x || !ev_y || !ev_p)) return EVS_ERR_ARG;
+  NoiseBatch b;
+  memset(&b, 0, sizeof(b));
+  b.a[0] = noise_args(p, L, ws, ev_t, ev_x, ev_y, ev_p, ev_key, meta_out);
+  return launch_noise(b, &L, 1, static_cast<cudaStream_t>(stream)) == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
+}
+
+size_t evs_noise_batch_workspace_bytes(const evs_noise_params* ps, int32_t nf) {
+  size_t total = 0;
+  for (int32_t f = 0; f < nf; ++f) {
+    NoiseLayout L;
+    if (!noise_layout(ps + f, &L)) return 0;
+    total += L.total;
+  }
+  return total;
+}
+
+evs_status evs_noise_batch(const evs_noise_params* ps, int32_t nf, int64_t* ev_t, uint16_t* ev_x, uint16_t* ev_y,
+                           int8_t* ev_p, int64_t ev_stride, int64_t* meta_out, void* ws, size_t ws_bytes,
+                           void* stream) {
+  if (!ps || nf < 0 || !ev_t || !ev_x || !ev_y || !ev_p || !meta_out || ev_stride < 0) return EVS_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int32_t f0 = 0; f0 < nf; f0 += kNoiseBatch) {
+    const int n = std::min<int>(kNoiseBatch, nf - f0);
+    NoiseBatch b;
+    memset(&b, 0, sizeof(b));
+    NoiseLayout Ls[kNoiseBatch];
+    size_t off = 0;
+    for (int f = 0; f < f0; ++f) {  // workspace offset of this batch's first frame
+      NoiseLayout L;
+      if (!noise_layout(ps + f, &L)) return EVS_ERR_ARG;
+      off += L.total;
+    }
+    for (int j = 0; j < n; ++j) {
+      const evs_noise_params* p = ps + f0 + j;
+      if (!noise_layout(p, &Ls[j]) || p->order != 0) return EVS_ERR_ARG;
+      if (!ws || ws_bytes < off + Ls[j].total) return EVS_ERR_WORKSPACE;
+      if (Ls[j].cap > ev_stride) return EVS_ERR_ARG;  // each frame's capacity must fit its row
+      const int64_t r = (int64_t)(f0 + j) * ev_stride;
+      b.a[j] = noise_args(p, Ls[j], static_cast<char*>(ws) + off, ev_t + r, ev_x + r, ev_y + r, ev_p + r,
+                          nullptr, meta_out + 4 * (int64_t)(f0 + j));
+      off += Ls[j].total;
+    }
+    if (launch_noise(b, Ls, n, st) != cudaSuccess) return EVS_ERR_CUDA;
+  }
+  return EVS_OK;
 }
 
 }  // extern "C"

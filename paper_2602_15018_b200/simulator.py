@@ -317,8 +317,9 @@ class EventSimulator:
         independent (exact int64 numerators, one rounding), so nothing is
         sorted or merged: the signal numerators come straight from the step's
         per-tile key regions (evs_step_voxel: one CTA per tile, shared-memory
-        accumulation; the bucket path uses its output rows), T noise launches
-        fill a pooled buffer, one segmented accumulation adds the noise, one
+        accumulation; the bucket path uses its output rows), one batched noise
+        launch set (evs_noise_batch) fills a pooled buffer with the T frames'
+        noise, one segmented accumulation adds it, one
         rounding, and one host read per window (the noise kernels' retry
         flags; a flagged frame is redone by the retrying path)."""
         import ctypes
@@ -377,7 +378,8 @@ class EventSimulator:
             cap = int(_noise_capacity)
         for p in params:
             p.capacity = cap
-        nws = max(int(L.evs_noise_workspace_bytes(ctypes.byref(p))) for p in params)
+        parr = (_lib.NoiseParams * T)(*params)
+        nws = int(L.evs_noise_batch_workspace_bytes(parr, T))
         pool = getattr(self, "_noise_pool", None)
         if pool is None or pool["t"].shape[0] < T or pool["t"].shape[1] < cap or pool["ws"].numel() < nws:
             pool = self._noise_pool = {
@@ -388,11 +390,10 @@ class EventSimulator:
                 "meta": torch.zeros((T, 4), dtype=torch.int64, device=self.device),
                 "ws": torch.empty(max(nws, 1), dtype=torch.uint8, device=self.device)}
         nt, nx, ny, npol, meta, nw = (pool[k] for k in ("t", "x", "y", "p", "meta", "ws"))
-        for f, p in enumerate(params):
-            rc = L.evs_noise(ctypes.byref(p), nt[f].data_ptr(), nx[f].data_ptr(), ny[f].data_ptr(),
-                             npol[f].data_ptr(), None, meta[f].data_ptr(), nw.data_ptr(), nw.numel(), st)
-            _lib.check(rc, "evs_noise")
         stride = nt.shape[1]
+        rc = L.evs_noise_batch(parr, T, nt.data_ptr(), nx.data_ptr(), ny.data_ptr(), npol.data_ptr(), stride,
+                               meta.data_ptr(), nw.data_ptr(), nw.numel(), st)
+        _lib.check(rc, "evs_noise_batch")
         vox(T, meta[:, 1].data_ptr(), 4, stride, nt.data_ptr(), nx.data_ptr(), ny.data_ptr(), npol.data_ptr(),
             _lib.EVS_VOXEL_FINALIZE)
         retry = meta[:T, 2:4].cpu().numpy()
