@@ -196,7 +196,9 @@ class EventSimulator:
         ev_h2d = [torch.cuda.Event() for _ in range(2)]
         ev_comp = [torch.cuda.Event() for _ in range(2)]
         ev_d2h = [torch.cuda.Event() for _ in range(2)]
-        scratch = [{}, {}]  # device staging of the packed segments, one per pool
+        if not hasattr(self, "_rh_scratch"):  # device staging of the packed segments, one per pool
+            self._rh_scratch = [{}, {}]       # (kept across calls: allocating it synchronises)
+        scratch = self._rh_scratch
         for e in ev_comp + ev_d2h:
             e.record(comp)
 
