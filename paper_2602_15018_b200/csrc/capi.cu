@@ -323,6 +323,10 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
     ts.bak_ref = g.bak_ref; ts.bak_last = g.bak_last;
     ts.ref = b->ref_log; ts.last = b->last_event_t; ts.sp = (int64_t)p->streams * P;
   }
+  if (ts.rows) {
+    e = launch_group_hist(ts, st);
+    if (e != cudaSuccess) return EVS_ERR_CUDA;
+  }
   e = launch_tilescan(ts, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(3);

@@ -164,6 +164,7 @@ struct StepVoxArgs {
 constexpr int kStepVoxMaxBins = 24;
 cudaError_t launch_step_voxel(const StepVoxArgs& a, cudaStream_t st);
 cudaError_t launch_step_hist(const StepVoxArgs& a, int S, int64_t lo, int64_t hi, int64_t* out, cudaStream_t st);
+cudaError_t launch_group_hist(const TileScanArgs& a, cudaStream_t st);
 cudaError_t launch_tilescan(const TileScanArgs& a, cudaStream_t st);
 cudaError_t launch_tile_order(const TileOrderArgs& a, cudaStream_t st);
 
