@@ -440,18 +440,18 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "traffic_note": "dram read+write bytes per step from ncu (profiles/r1_step_traffic.json)",
-                     "kernel": "evs_step (k_prologue + k_generate + k_tilescan + k_tile_order), "
+                     "kernel": "evs_step (k_prologue + k_generate + k_group_hist + k_tilescan + k_tile_order), "
                                "device time per step of the timed region",
                      "algorithmic_bytes_per_step": B,
                      "stage_ms_per_step": {"prologue": stage_ms[0], "generate": stage_ms[1],
-                                           "tilescan": stage_ms[2], "order": stage_ms[3]},
+                                           "group_hist+tilescan": stage_ms[2], "order": stage_ms[3]},
                      "generate_only": {"bytes": gen_bytes, "achieved": gen_achieved,
                                        "frac": gen_achieved / peak}},
         "per_frame_launch": per_frame,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "e2e_per_frame_api": e2e_frame,
-        "gpu_launches": K * 4 + reps,
+        "gpu_launches": K * 5 + reps,  # five kernels per evs_step (+ one clock init per graph replay)
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

@@ -7,6 +7,6 @@ timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; e
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_prologue|k_generate|k_tilescan|k_tile_order" -s 24 -c 40 --csv --log-file gpurun_out/launches.csv python bench.py --steps 10 --warmup 3 --compare-t1 0 --cpu-seconds 0 > gpurun_out/ncu_launch_bench.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_generate|k_tile_order" -s 8 -c 2 -o gpurun_out/prof python bench.py --steps 4 --warmup 3 --compare-t1 0 --cpu-seconds 0 > gpurun_out/ncu_full.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_prologue|k_generate|k_group_hist|k_tilescan|k_tile_order" -s 30 -c 50 --csv --log-file gpurun_out/launches.csv python bench.py --steps 10 --warmup 3 --compare-t1 0 --cpu-seconds 0 > gpurun_out/ncu_launch_bench.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_generate|k_group_hist|k_tile_order" -s 12 -c 3 -o gpurun_out/prof python bench.py --steps 4 --warmup 3 --compare-t1 0 --cpu-seconds 0 > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out
