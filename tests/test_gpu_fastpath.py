@@ -141,9 +141,37 @@ def test_random_inputs_fast_equals_exact_path():
         assert np.array_equal(a[1], oref) and np.array_equal(a[2], olast)
 
 
-def test_overflow_tiles_sorted_by_fixup():
-    """> 3 crossings per pixel across whole tiles: the tile lists overflow shared
-    memory and go through the overflow area + fixup sort."""
+def test_tile_order_overflow_area_within_capacity():
+    """~6 crossings per pixel (under the capacity): every tile-order region
+    overflows (> 4096 events per 1024-pixel tile) into the overflow area, whose
+    keys K2 and k_group_hist then read."""
+    rng = np.random.default_rng(4)
+    S, T, H, W = 1, 2, 64, 96
+    L0 = rng.uniform(-3.0, -2.0, (H, W))
+    ref0 = L0.astype(np.float32)[None]
+    f1 = oracle.frame_from_log(L0 + rng.uniform(0.055, 0.075, (H, W)))
+    f2 = oracle.frame_from_log(L0 + rng.uniform(0.0, 0.02, (H, W)))
+    frames = np.stack([[f1, f2]]).astype(np.float32)
+    last0 = np.full((1, H, W), -100, np.int64)
+    thp = np.full((1, H, W), 0.01, np.float32)
+    thn = np.full((1, H, W), 0.011, np.float32)
+    cap = 8 * H * W
+    for refr in (0, 3):
+        segs, ref, last = _run(frames, ref0, last0, thp, thn, refr, cap, (0.01, 0.011), legacy=True)
+        exp, oref, olast = _oracle_segments(frames, ref0, last0, thp, thn, refr, cap)
+        assert len(exp[0]) > 5 * H * W  # > 4096 per 1024-pixel tile
+        _same(segs, exp)
+        assert np.array_equal(ref, oref) and np.array_equal(last, olast)
+
+
+@PATHS
+def test_overflow_tiles_sorted_by_fixup(bucket):
+    """> 3 crossings per pixel across whole tiles: the bucket path's tile lists
+    overflow shared memory (overflow area + fixup sort).  The first frame lies
+    far above its capacity, which the tile-order path reports instead
+    (its overflow area holds at most the capacity + a few tiles)."""
+    if not bucket:
+        pytest.skip("tile-order path: see test_tile_order_overflow_area_within_capacity")
     rng = np.random.default_rng(2)
     S, T, H, W = 1, 2, 64, 96
     L0 = rng.uniform(-4.0, -3.0, (H, W))
@@ -156,7 +184,7 @@ def test_overflow_tiles_sorted_by_fixup():
     thn = np.full((1, H, W), 0.011, np.float32)
     cap = 8 * H * W
     for refr in (0, 20):
-        segs, ref, last = _run(frames, ref0, last0, thp, thn, refr, cap, (0.01, 0.011))
+        segs, ref, last = _run(frames, ref0, last0, thp, thn, refr, cap, (0.01, 0.011), legacy=not bucket)
         exp, oref, olast = _oracle_segments(frames, ref0, last0, thp, thn, refr, cap)
         assert max(len(e) for e in exp) > 3 * H * W  # really overflowed
         _same(segs, exp)
