@@ -1,10 +1,11 @@
 // extern "C" entry points of libevsim_b200.so (see include/evsim_b200.h).
 //
-// One evs_step = k_prologue (validate + clock + counters) -> k_generate (K1,
-// per-tile event regions) -> k_tilescan (tile bases, counts, capacity, column
-// scan of the t_rel histogram rows) -> k_tile_order (K2: canonical order, or
+// One evs_step = k_prologue (clock + counters; validation for calls of < 4
+// frames) -> k_generate (K1, per-tile event regions) -> k_group_hist (t_rel
+// histogram rows of the tile groups) -> k_tilescan (tile bases, counts,
+// capacity, column scan of the rows) -> k_tile_order (K2: canonical order, or
 // pixel-major compaction for the serial API) [-> generic onesweep passes when
-// t_now - t_prev exceeds 2^11 us].
+// t_now - t_prev exceeds 2^11 us].  EVS_PATH=bucket selects fast_path.cu.
 #include <cuda_runtime.h>
 
 #include <cstdint>

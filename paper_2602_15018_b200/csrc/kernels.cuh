@@ -61,7 +61,8 @@ struct GenArgs {
   int ntiles;  // tiles per stream frame
   const StepDesc* desc;  // non-null: t0 / epoch come from the device clock
   // per tile-group t_rel histogram rows (canonical order, pass 0):
-  // rows[seg][group][NB], group = tile / kGroupTiles; group_base[seg][group]
+  // rows[seg][group][NB], group = tile / gt -- filled by k_group_hist, carried
+  // here for the later passes' arguments (K1 itself does not touch them)
   uint32_t* rows;
   int64_t* group_base;
   int ngroups;
