@@ -286,8 +286,9 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   g.gt = L.gt;
   {
     // split each tile's T frames into chunks so the grid is >= ~8 waves of
-    // resident K1 CTAs (3 per SM): the tail wave then lasts one short chunk
-    const int64_t resident = (int64_t)sm_count_current() * 3;
+    // resident K1 CTAs (4 per SM; HD T=50: 6 chunks of 9 frames, measured best
+    // against 4, 5 and 8): the tail wave then lasts one short chunk
+    const int64_t resident = (int64_t)sm_count_current() * 4;
     const int64_t tiles = (int64_t)p->streams * L.ntiles;
     int64_t nch = (8 * resident + tiles - 1) / tiles;
     if (nch > p->frames) nch = p->frames;
