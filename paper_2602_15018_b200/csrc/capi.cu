@@ -291,7 +291,9 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
     const int64_t resident = (int64_t)sm_count_current() * 4;
     const int64_t tiles = (int64_t)p->streams * L.ntiles;
     int64_t nch = (8 * resident + tiles - 1) / tiles;
-    if (nch > p->frames) nch = p->frames;
+    // >= 2 frames per chunk: one-frame chunks of a small sensor serialise on
+    // the chunk hand-off (DAVIS T=50: 50 chunks ran 17 % slower than 25)
+    if (nch > (p->frames + 1) / 2) nch = (p->frames + 1) / 2;
     if (nch > 255) nch = 255;
     if (nch < 1) nch = 1;
     g.tc = (int)((p->frames + nch - 1) / nch);
