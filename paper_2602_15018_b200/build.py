@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libevsim_b200.so")
-SOURCES = ["k1_list.cu", "fast_path.cu", "order.cu", "sort.cu", "noise.cu", "represent.cu", "render.cu", "capi.cu"]
+SOURCES = ["k1_list.cu", "order.cu", "sort.cu", "noise.cu", "represent.cu", "render.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

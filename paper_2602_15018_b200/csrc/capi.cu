@@ -5,7 +5,7 @@
 // histogram rows of the tile groups) -> k_tilescan (tile bases, counts,
 // capacity, column scan of the rows) -> k_tile_order (K2: canonical order, or
 // pixel-major compaction for the serial API) [-> generic onesweep passes when
-// t_now - t_prev exceeds 2^11 us].  EVS_PATH=bucket selects fast_path.cu.
+// t_now - t_prev exceeds 2^11 us].
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -15,7 +15,6 @@
 #include "../../include/evsim_b200.h"
 #include "common.cuh"
 #include "kernels.cuh"
-#include "fast_path.cuh"
 
 using namespace evs;
 
@@ -37,45 +36,11 @@ int sm_count_current() {
 
 struct StepLayout {
   int nseg, ntiles, npass, bits, NB, ngroups, gt;
-  int64_t max_tiles2, ovf_cap;
+  int64_t max_tiles2, ovf_lim, ovf_cap, n2;
   size_t chunk_flag;
   size_t ctr, desc, zero2, region, tile_count, tile_ovf, tile_base, ovf_area, rows, tot, hist, gstart,
-      seg_tbase, seg_tile_prefix, status2, keysA, keysB, total, bak_ref, bak_last;
-  // fast canonical path (fast_path.cu)
-  bool fast;
-  int fG, fntiles, fnbk, fmaxp;
-  int64_t n2;
-  size_t fkeys, frows, fsrc, fsnapr, fsnapl, fareau, fareas, fitems, flim, fredon, fpieces, fnpieces, fpcnt;
+      seg_tbase, seg_dt, seg_tile_prefix, status2, keysA, keysB, total, bak_ref, bak_last, snap_ref, snap_last;
 };
-
-// Fast path: canonical order, t_now - t_prev <= 2048 us, P < 2^24.  Tiles of
-// G <= 2048 pixels (a multiple of 32, so tiles start on 32-pixel chunk
-// boundaries) sized so the S*ntiles CTAs fill whole waves of 2 CTAs per SM.
-bool fast_shape(const evs_step_params* p, int64_t P, int64_t mdt, int* G, int* ntiles, int* nbk) {
-  if (p->order != EVS_ORDER_CANONICAL || mdt < 1 || mdt > 8 * kFMaxBuckets) return false;
-  // the bucket path is opt-in (EVS_PATH=bucket): on the HD benchmark the
-  // tile-order path is faster
-  const char* path = getenv("EVS_PATH");
-  if (!(path && path[0] == 'b')) return false;
-  const char* force = getenv("EVS_FORCE_LEGACY");
-  if (force && force[0] == '1') return false;
-  if (P >= (1ll << 24) || (int64_t)p->frames * mdt >= (1ll << 29)) return false;
-  if (p->refractory_us >= (1ll << 29)) return false;
-  const int64_t slots = (int64_t)kFCtasPerSm * sm_count_current();
-  const int64_t S = p->streams;
-  const int64_t min_tiles = (P + kFGmax - 1) / kFGmax;
-  const int64_t waves = (S * min_tiles + slots - 1) / slots;
-  int64_t nt = (waves * slots + S - 1) / S;
-  int64_t g = (P + nt - 1) / nt;
-  g = (g + 31) / 32 * 32;
-  if (g > kFGmax) g = kFGmax;
-  nt = (P + g - 1) / g;
-  if (nt > kFMaxTiles) return false;
-  *G = (int)g;
-  *ntiles = (int)nt;
-  *nbk = (int)((mdt + 7) / 8);
-  return true;
-}
 
 __global__ void k_clock_init(StepDesc* d, int64_t t0, uint32_t epoch) {
   d->next_t0 = t0;
@@ -112,23 +77,26 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
       if ((int64_t)((L->ntiles + g - 1) / g) * L->nseg >= want) { L->gt = g; break; }
   }
   L->ngroups = (L->ntiles + L->gt - 1) / L->gt;
-  // overflow area (lanes with > kSlotsPerLane events): the kept events of a
-  // frame never exceed the capacity, so capacity + one tile is always enough
-  L->ovf_cap = p->capacity + (int64_t)kTileCap * (1 + L->ntiles / 4);
+  // spill area per segment: [0, ovf_lim) is claimed by K1 tiles whose keys do
+  // not fit their region (atomic cursor, arrival order); a tile that finds it
+  // full keeps only its count and a pre-frame state snapshot, and k_group_hist
+  // regenerates it into [ovf_lim, ovf_lim + capacity) when it lies inside the
+  // kept prefix (the kept events of a frame never exceed the capacity)
+  L->ovf_lim = (int64_t)kTileCap * (1 + L->ntiles / 4);
+  L->ovf_cap = L->ovf_lim + p->capacity;
   const size_t ns = (size_t)L->nseg, nt = (size_t)L->ntiles;
   size_t off = 0;
   L->ctr = off; off = align_up(off + 64 * sizeof(uint32_t));
   L->desc = off; off = align_up(off + sizeof(StepDesc));
-  const bool fast_early = fast_shape(p, P, canon ? (p->max_dt > 0 ? p->max_dt : p->tick) : 0, &L->fG,
-                                     &L->fntiles, &L->fnbk);
-  // zeroed by the prologue: ovf_cursor[nseg] + err (+ fast path: bucket totals [nseg][nbk] u32)
-  L->n2 = (int64_t)ns + 1 + (fast_early ? ((int64_t)ns * L->fnbk + 1) / 2 : 0);
+  // zeroed by the prologue: spill cursors [nseg], K1 error word, K1 CTA ticket
+  L->n2 = (int64_t)ns + 2;
   L->zero2 = off; off = align_up(off + (size_t)L->n2 * 8);
   L->chunk_flag = off; off = align_up(off + (size_t)p->streams * nt * 8);
   L->tile_count = off; off = align_up(off + ns * nt * 8);
   L->tile_ovf = off; off = align_up(off + ns * nt * 8);
   L->tile_base = off; off = align_up(off + ns * nt * 8);
   L->seg_tbase = off; off = align_up(off + ns * 8);
+  L->seg_dt = off; off = align_up(off + ns * 8);
   L->rows = off; off = align_up(off + (canon ? ns * L->ngroups * L->NB * 4 : 0));
   L->tot = off; off = align_up(off + ns * L->NB * 4);
   L->hist = off; off = align_up(off + (L->npass > 1 ? ns * L->npass * kHistReps * L->NB * 4 : 0));
@@ -137,32 +105,13 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   L->status2 = off; off = align_up(off + ns * L->max_tiles2 * L->NB * 8);
   L->keysA = off; off = align_up(off + (canon && L->npass > 1 ? ns * p->capacity * 8 : 0));
   L->keysB = off; off = align_up(off + (canon && L->npass > 1 ? ns * p->capacity * 8 : 0));
-  const bool fast_sel = fast_shape(p, P, canon ? (p->max_dt > 0 ? p->max_dt : p->tick) : 0, &L->fG,
-                                   &L->fntiles, &L->fnbk);
-  const bool bak = !fast_sel && p->frames >= 4;  // fused validation (step_impl)
+  const bool bak = p->frames >= 4;  // fused validation (step_impl)
   L->bak_ref = off; off = align_up(off + (bak ? (size_t)p->streams * P * 4 : 0));
   L->bak_last = off; off = align_up(off + (bak ? (size_t)p->streams * P * 8 : 0));
-  L->region = off; off = align_up(off + (fast_sel ? 0 : ns * nt * kTileCap * 8));
-  L->ovf_area = off; off = align_up(off + (fast_sel ? 0 : ns * (size_t)L->ovf_cap * 8));
-  L->fast = fast_shape(p, P, canon ? (p->max_dt > 0 ? p->max_dt : p->tick) : 0, &L->fG, &L->fntiles, &L->fnbk);
-  if (L->fast) {
-    const size_t fnt = (size_t)L->fntiles;
-    const size_t cap = (size_t)(p->capacity > 0 ? p->capacity : 1);
-    L->fkeys = off; off = align_up(off + ns * fnt * kFListCap * 4);
-    L->frows = off; off = align_up(off + ns * (L->fnbk + 1) * fnt * 4);
-    L->fsrc = off; off = align_up(off + ns * fnt * 8);
-    L->fsnapr = off; off = align_up(off + ns * fnt * L->fG * 4);
-    L->fsnapl = off; off = align_up(off + ns * fnt * L->fG * 4);
-    L->fareau = off; off = align_up(off + ns * cap * 4);
-    L->fareas = off; off = align_up(off + ns * cap * 4);
-    L->fitems = off; off = align_up(off + ns * fnt * 8);
-    L->flim = off; off = align_up(off + ns * fnt * 4);
-    L->fredon = off; off = align_up(off + ns * 4);
-    L->fmaxp = L->fnbk + 2 * (int)((cap + kOCap - 1) / kOCap) + 2;
-    L->fpieces = off; off = align_up(off + ns * (size_t)L->fmaxp * 8 * 4);
-    L->fnpieces = off; off = align_up(off + ns * 4);
-    L->fpcnt = off; off = align_up(off + ns * (size_t)L->fmaxp * 8 * 4);
-  }
+  L->region = off; off = align_up(off + ns * nt * kTileCap * 8);
+  L->ovf_area = off; off = align_up(off + ns * (size_t)L->ovf_cap * 8);
+  L->snap_ref = off; off = align_up(off + ns * nt * kGenTile * 4);
+  L->snap_last = off; off = align_up(off + ns * nt * kGenTile * 4);
   L->total = off;
   return true;
 }
@@ -197,7 +146,10 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
                             size_t ws_bytes, void* stream, void* const* evs, int nev) {
   StepLayout L;
   if (!step_layout(p, &L) || !b) return EVS_ERR_ARG;
-  if (p->log_eps <= 0 || p->refractory_us < 0 || p->capacity >= (1ll << 32)) return EVS_ERR_ARG;
+  // refractory periods are compared in int32 against last-event times clamped
+  // to [-2^30, 2^30] relative to the frame start: exact for refractory < 2^30 us
+  if (p->log_eps <= 0 || p->refractory_us < 0 || p->refractory_us >= (1ll << 30) || p->capacity >= (1ll << 32))
+    return EVS_ERR_ARG;
   if (!b->frames || !b->ref_log || !b->last_event_t || !b->counts || !b->dropped ||
       !b->reservations || !b->bad_pixel)
     return EVS_ERR_ARG;
@@ -221,50 +173,12 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   // the tile-order path validates inside K1 (fused: K1 backs up the state it
   // overwrites, 12 B/px) when the call has >= 4 frames per stream; shorter calls
   // read the frames once in the prologue (4 B/px per frame) instead
-  const bool fuse_val = p->validate && !L.fast && p->frames >= 4;
+  const bool fuse_val = p->validate && p->frames >= 4;
   cudaError_t e = launch_prologue(b->frames, (int64_t)L.nseg * P, P, fuse_val ? 0 : p->validate, b->bad_pixel,
                                   b->reservations, L.nseg, desc, (int64_t)p->frames * p->tick, zero2,
                                   L.n2, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(1);
-
-  if (L.fast) {
-    FastArgs fa;
-    memset(&fa, 0, sizeof(fa));
-    fa.S = p->streams; fa.T = p->frames; fa.W = p->width; fa.P = P;
-    fa.G = L.fG; fa.ntiles = L.fntiles; fa.nbk = L.fnbk;
-    fa.vec = (P % 4 == 0) && ((uintptr_t)b->frames % 16 == 0) && ((uintptr_t)b->ref_log % 16 == 0) &&
-             ((uintptr_t)b->last_event_t % 16 == 0) &&
-             (b->th_pos == nullptr || (((uintptr_t)b->th_pos % 16 == 0) && ((uintptr_t)b->th_neg % 16 == 0)));
-    fa.log_eps = p->log_eps; fa.log_eps_f = (float)p->log_eps;
-    fa.refr = (int)p->refractory_us;
-    fa.thp_u = p->th_pos_uniform; fa.thn_u = p->th_neg_uniform;
-    fa.rthp_u = (float)(1.0 / (double)p->th_pos_uniform);
-    fa.rthn_u = (float)(1.0 / (double)p->th_neg_uniform);
-    fa.frames = b->frames; fa.t_bounds = b->t_bounds; fa.t0 = p->t0; fa.tick = p->tick; fa.desc = desc;
-    fa.ref = b->ref_log; fa.last = b->last_event_t; fa.thp = b->th_pos; fa.thn = b->th_neg;
-    fa.bad = b->bad_pixel; fa.seg_res = b->reservations;
-    fa.keys = at<uint32_t>(ws, L.fkeys); fa.rows = at<uint32_t>(ws, L.frows);
-    fa.tile_src = at<int64_t>(ws, L.fsrc);
-    fa.snap_ref = at<float>(ws, L.fsnapr); fa.snap_last = at<int>(ws, L.fsnapl);
-    fa.area_unsorted = at<uint32_t>(ws, L.fareau); fa.area_sorted = at<uint32_t>(ws, L.fareas);
-    fa.redo_items = at<int>(ws, L.fitems); fa.redo_lim = at<int>(ws, L.flim); fa.redo_n = at<int>(ws, L.fredon);
-    fa.btot = reinterpret_cast<uint32_t*>(zero2 + L.nseg + 1);
-    fa.pieces = at<int>(ws, L.fpieces); fa.npieces = at<int>(ws, L.fnpieces);
-    fa.pcnt = at<uint32_t>(ws, L.fpcnt); fa.maxp = L.fmaxp;
-    fa.cap = p->capacity; fa.out_count = b->counts; fa.out_dropped = b->dropped;
-    fa.seg_stride = p->capacity;
-    fa.out_t = b->ev_t; fa.out_x = b->ev_x; fa.out_y = b->ev_y; fa.out_p = b->ev_p;
-    if (launch_fast_gen(fa, st) != cudaSuccess) return EVS_ERR_CUDA;
-    mark(2);
-    if (launch_fast_fix(fa, L.nseg, st) != cudaSuccess) return EVS_ERR_CUDA;
-    if (launch_fast_redo(fa, L.nseg, st) != cudaSuccess) return EVS_ERR_CUDA;
-    if (launch_fast_plan(fa, L.nseg, st) != cudaSuccess) return EVS_ERR_CUDA;
-    mark(3);
-    if (launch_fast_order(fa, L.nseg, st) != cudaSuccess) return EVS_ERR_CUDA;
-    mark(4);
-    return EVS_OK;
-  }
 
   GenArgs g;
   memset(&g, 0, sizeof(g));
@@ -306,7 +220,12 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   g.ovf_area = at<uint64_t>(ws, L.ovf_area);
   g.ovf_cursor = reinterpret_cast<unsigned long long*>(zero2);
   g.ovf_cap = L.ovf_cap;
+  g.ovf_lim = L.ovf_lim;
   g.err = zero2 + L.nseg;
+  g.ticket = reinterpret_cast<unsigned int*>(zero2 + L.nseg + 1);
+  g.seg_dt = at<int64_t>(ws, L.seg_dt);
+  g.snap_ref = at<float>(ws, L.snap_ref);
+  g.snap_last = at<int32_t>(ws, L.snap_last);
   g.fuse_validate = fuse_val ? 1 : 0;
   g.bad_rw = b->bad_pixel;
   g.bak_ref = at<float>(ws, L.bak_ref);
@@ -321,16 +240,22 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   ts.gt = L.gt;
   ts.tile_count = g.tile_count; ts.tile_ovf = g.tile_ovf; ts.region = g.region; ts.ovf_area = g.ovf_area;
   ts.ovf_cap = L.ovf_cap; ts.tile_base = at<int64_t>(ws, L.tile_base);
+  // regeneration of the tiles K1 could not store (k_group_hist)
+  ts.ovf_lim = L.ovf_lim; ts.ovf_cursor = g.ovf_cursor; ts.err_rw = g.err;
+  ts.frames = b->frames; ts.T = p->frames; ts.W = p->width; ts.P = P;
+  ts.thp = b->th_pos; ts.thn = b->th_neg; ts.thp_u = p->th_pos_uniform; ts.thn_u = p->th_neg_uniform;
+  ts.log_eps = p->log_eps; ts.refr = (int)p->refractory_us;
+  ts.seg_tbase = g.seg_tbase; ts.seg_dt = g.seg_dt; ts.snap_ref = g.snap_ref; ts.snap_last = g.snap_last;
   ts.rows = g.rows; ts.tot = at<uint32_t>(ws, L.tot);
   ts.out_count = b->counts; ts.out_dropped = b->dropped; ts.bad = b->bad_pixel; ts.err = g.err;
   if (fuse_val) {
     ts.bak_ref = g.bak_ref; ts.bak_last = g.bak_last;
     ts.ref = b->ref_log; ts.last = b->last_event_t; ts.sp = (int64_t)p->streams * P;
   }
-  if (ts.rows) {
-    e = launch_group_hist(ts, st);
-    if (e != cudaSuccess) return EVS_ERR_CUDA;
-  }
+  // (pixel-major order: no histogram rows, only the regeneration of tiles K1
+  // could not store)
+  e = launch_group_hist(ts, st);
+  if (e != cudaSuccess) return EVS_ERR_CUDA;
   e = launch_tilescan(ts, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(3);
@@ -431,7 +356,6 @@ evs_status evs_step_voxel(const evs_step_params* p, const evs_step_buffers* b, c
   if (!ws || ws_bytes < L.total) return EVS_ERR_WORKSPACE;
   if (stream_index < 0 || stream_index >= p->streams || t1 <= t0 || bins < 2 || bins > kStepVoxMaxBins)
     return EVS_ERR_ARG;
-  if (L.fast) return EVS_ERR_UNSUPPORTED;  // bucket path: no per-tile regions
   const int64_t P = (int64_t)p->height * p->width;
   const bool fin = (flags & EVS_VOXEL_FINALIZE) != 0;
   if (fin ? !out : (!voxel_ws || voxel_ws_bytes < (size_t)bins * P * sizeof(long long))) return EVS_ERR_ARG;
@@ -450,7 +374,6 @@ evs_status evs_step_histogram(const evs_step_params* p, const evs_step_buffers* 
   if (!step_layout(p, &L) || !b || !b->bad_pixel || !out) return EVS_ERR_ARG;
   if (!ws || ws_bytes < L.total) return EVS_ERR_WORKSPACE;
   if (p->streams > 65535) return EVS_ERR_ARG;
-  if (L.fast) return EVS_ERR_UNSUPPORTED;
   StepVoxArgs a;
   step_regions(p, b, L, ws, &a);
   return launch_step_hist(a, p->streams, t_end - window_us, t_end, out, static_cast<cudaStream_t>(stream)) ==

@@ -73,10 +73,15 @@ struct GenArgs {
   uint64_t* region;          // [nseg][ntiles][kTileCap] pixel-major keys
   int64_t* tile_count;       // [nseg][ntiles] events of the tile (before capacity)
   int64_t* tile_ovf;         // [nseg][ntiles] -1, or offset into ovf_area (lane slot overflow)
-  uint64_t* ovf_area;        // [nseg][ovf_cap]
+  uint64_t* ovf_area;        // [nseg][ovf_cap] spill: K1 claims [0, ovf_lim), regenerated tiles follow
   unsigned long long* ovf_cursor;  // [nseg], zeroed by the prologue
-  int64_t ovf_cap;
-  int64_t* err;              // [1] bit 0: overflow area exhausted, bit 1: corrupt level (> kMaxPixelCrossings)
+  int64_t ovf_cap, ovf_lim;
+  int64_t* err;              // [1] bit 1: corrupt level (> kMaxPixelCrossings)
+  unsigned int* ticket;      // CTA ticket (zeroed by the prologue): work in dispatch order
+  int64_t* seg_dt;           // [S*T] t_now - t_prev of each segment
+  // tiles that found the spill area full: pre-frame state for their regeneration
+  float* snap_ref;           // [nseg][ntiles][kGenTile]
+  int32_t* snap_last;        // [nseg][ntiles][kGenTile] last event - t_prev, clamped to [-2^30, 2^30]
   int gt;                    // tiles per group (histogram row)
   // frame chunking: block b handles chunk c = b / (S*ntiles) = frames
   // [c*tc, min(T, (c+1)*tc)) of its tile; chunk c waits for chunk c-1 of the
@@ -94,6 +99,7 @@ struct GenArgs {
 };
 
 constexpr int kSlotsPerLane = 16;
+constexpr int64_t kTileRedo = -3;  // tile_ovf: K1 kept only the count (k_group_hist regenerates)
 constexpr int kTileCap = kSlotsPerLane * kGenThreads;  // keys per tile region
 
 struct TileScanArgs {
@@ -110,8 +116,25 @@ struct TileScanArgs {
   int64_t* out_count;
   int64_t* out_dropped;
   const int64_t* bad;
-  const int64_t* err;         // K1 errors -> out_dropped = -1 (overflow area) / -2 (corrupt level)
+  const int64_t* err;         // K1 errors -> out_dropped = -2 (corrupt level)
   int gt;
+  // regeneration of tiles K1 could not store (tile_ovf == kTileRedo, or
+  // >= ovf_lim once regenerated): k_group_hist, when ovf_cursor[seg] > ovf_lim
+  int64_t ovf_lim;
+  const unsigned long long* ovf_cursor;
+  int64_t* err_rw;
+  const float* frames;
+  int T, W;
+  int64_t P;
+  const float* thp;
+  const float* thn;
+  float thp_u, thn_u;
+  double log_eps;
+  int refr;
+  const int64_t* seg_tbase;
+  const int64_t* seg_dt;
+  const float* snap_ref;
+  const int32_t* snap_last;
   // fused validation: restore the state from the backup when a frame was invalid
   const float* bak_ref;
   const int64_t* bak_last;
@@ -217,7 +240,7 @@ struct HistArgs {
   uint32_t* hist;          // [nseg][npass][R][NB]
 };
 
-// host launchers (kernels.cu)
+// host launchers (k1_list.cu, order.cu)
 cudaError_t launch_prologue(const float* frames, int64_t nframes, int64_t P, int validate,
                             int64_t* bad, int64_t* seg_res, int nseg, StepDesc* desc,
                             int64_t t_advance, int64_t* zero2, int64_t n2, cudaStream_t st);

@@ -2,7 +2,7 @@
 //
 //   k_prologue  : frame validation (reference ValueError semantics,
 //                 model.py:28-39) + per-call accumulator reset.
-//   (k_generate, the fused K1, lives in generate.cu)
+//   (k_generate, K1, and the tile-order K2 live in k1_list.cu)
 //   k_plan      : per-segment counts / capacity (parallel.py:261-273),
 //                 histogram reduction + bin starts, work list for k_order.
 //   k_hist      : digit histograms of a key array (generic sort passes).

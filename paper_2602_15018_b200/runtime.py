@@ -36,6 +36,10 @@ class StepEngine:
     def __init__(self, shape: StepShape, device):
         import torch
 
+        if int(shape.refractory_us) >= (1 << 30):
+            # the kernels compare refractory periods in int32 against last-event
+            # times clamped to +-2^30 us around the frame start
+            raise ValueError("refractory_us must be < 2**30 us (about 17.9 minutes) on the GPU path")
         _lib.require_cuda()
         self.shape = shape
         self.device = device
@@ -182,9 +186,6 @@ class StepEngine:
             raise _lib.NativeError("a pixel would cross more than 2**20 thresholds in one frame: an infinite "
                                    "intensity (with validate=False) or a reference level (ref_log) far outside "
                                    "the log range of [0, 1] intensities")
-        if int(host[-1]) == _lib.NO_BAD and (host[nseg:2 * nseg] < 0).any():
-            raise _lib.NativeError("event overflow area exhausted (a frame far above its capacity "
-                                   "concentrated > 4 events/pixel in many tiles); raise max_events_per_frame")
         return host[:nseg], host[nseg:2 * nseg], host[2 * nseg:3 * nseg], int(host[-1])
 
     def reset_bad(self) -> None:

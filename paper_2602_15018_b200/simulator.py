@@ -97,14 +97,37 @@ class EventSimulator:
         self.step_index = 0
 
     # -- stepping --------------------------------------------------------------
+    def _check_frames(self, frames, device: bool = True):
+        """The kernels read S*T*H*W float32 values through a raw pointer: reject
+        anything else before launching.  Returns the [S, T, H, W] view."""
+        import torch
+
+        full = (self.S, self.T, self.H, self.W)
+        if device:
+            if not isinstance(frames, torch.Tensor):
+                raise TypeError("frames must be a CUDA float32 tensor (use step_host for host arrays)")
+            if frames.dtype != torch.float32:
+                raise ValueError(f"frames must be float32, got {frames.dtype}")
+            if frames.device != self.device:
+                raise ValueError(f"frames must be on {self.device}, got {frames.device}")
+            if not frames.is_contiguous():
+                raise ValueError("frames must be contiguous")
+        shape = tuple(frames.shape)
+        if shape == (self.S, self.H, self.W) and self.T == 1:
+            return frames.unsqueeze(1) if device else frames[:, None]
+        if shape != full:
+            raise ValueError(f"frames shape {shape} != (streams, frames_per_step, height, width) = {full}"
+                             + (" (or (streams, height, width) when frames_per_step == 1)" if self.T == 1 else ""))
+        return frames
+
     def step(self, frames, validate: bool = True, sync: bool = False, stage_events=None):
-        """Advance every stream by T frames.  frames: float32 CUDA tensor [S, T, H, W]
-        (or [S, H, W] when T == 1).  Asynchronous unless sync=True."""
+        """Advance every stream by T frames.  frames: contiguous float32 CUDA tensor
+        [S, T, H, W] on this simulator's device (or [S, H, W] when T == 1).
+        Asynchronous unless sync=True."""
         eng = self.engine
         assert eng is not None, "call reset() first"
-        if frames.dim() == 3:
-            frames = frames.unsqueeze(1)
-        eng.launch(frames.contiguous(), self.ref, self.last, self.thp, self.thn, t0=self.t_next, tick=self.tick,
+        frames = self._check_frames(frames)
+        eng.launch(frames, self.ref, self.last, self.thp, self.thn, t0=self.t_next, tick=self.tick,
                    validate=validate, stage_events=stage_events)
         self.t_next += self.T * self.tick
         self.step_index += 1
@@ -141,9 +164,7 @@ class EventSimulator:
         from .events.types import EventBatch
         from .runtime import PinnedPool, compact_launch, d2h_packed
 
-        fr = np.ascontiguousarray(frames_host, np.float32)
-        if fr.ndim == 3:
-            fr = fr[:, None]
+        fr = self._check_frames(np.ascontiguousarray(frames_host, np.float32), device=False)
         dfr = torch.from_numpy(fr).to(self.device)
         self.step(dfr, validate=validate)
         e = self.engine
@@ -203,9 +224,7 @@ class EventSimulator:
             e.record(comp)
 
         def upload(i, win):
-            fr = np.ascontiguousarray(win, np.float32)
-            if fr.ndim == 3:
-                fr = fr[:, None]
+            fr = self._check_frames(np.ascontiguousarray(win, np.float32), device=False)
             with torch.cuda.stream(h2d):
                 h2d.wait_event(ev_comp[i % 2])  # window i-2 has finished reading this buffer
                 fbuf[i % 2].copy_(torch.from_numpy(fr), non_blocking=True)
@@ -276,7 +295,8 @@ class EventSimulator:
     # -- CUDA graph replay -------------------------------------------------------
     def capture(self, frame_windows) -> None:
         """Capture one graph stepping through `frame_windows` ([S, T, H, W] each) in order."""
-        self.engine.capture(list(frame_windows), self.ref, self.last, self.thp, self.thn, tick=self.tick,
+        frame_windows = [self._check_frames(w) for w in frame_windows]
+        self.engine.capture(frame_windows, self.ref, self.last, self.thp, self.thn, tick=self.tick,
                             t0=self.t_next)
         self._graph_len = len(frame_windows)
 
@@ -319,7 +339,7 @@ class EventSimulator:
         independent (exact int64 numerators, one rounding), so nothing is
         sorted or merged: the signal numerators come straight from the step's
         per-tile key regions (evs_step_voxel: one CTA per tile, shared-memory
-        accumulation; the bucket path uses its output rows), one batched noise
+        accumulation), one batched noise
         launch set (evs_noise_batch) fills a pooled buffer with the T frames'
         noise, one segmented accumulation adds it, one
         rounding, and one host read per window (the noise kernels' retry
@@ -351,18 +371,12 @@ class EventSimulator:
             _lib.check(rc, "evs_voxel_segments")
 
         def signal(flags):
-            # from the step's per-tile regions (shared-memory accumulation, every
-            # pixel written); the bucket path has none: the output rows instead
+            # from the step's per-tile regions (shared-memory accumulation, every pixel written)
             fin = flags & _lib.EVS_VOXEL_FINALIZE
             rc = L.evs_step_voxel(ctypes.byref(e.params), ctypes.byref(e.bufs), e.workspace.data_ptr(),
                                   e.workspace.numel(), s, t0, t1, bins, fin, out.data_ptr(), ws.data_ptr(),
                                   ws.numel(), st)
-            if rc == _lib.EVS_ERR_UNSUPPORTED:
-                vox(T, e.info[0, g0:].data_ptr(), 1, e.ev_t.shape[1], e.ev_t[g0].data_ptr(),
-                    e.ev_x[g0].data_ptr(), e.ev_y[g0].data_ptr(), e.ev_p[g0].data_ptr(),
-                    flags | _lib.EVS_VOXEL_CLEAR)
-            else:
-                _lib.check(rc, "evs_step_voxel")
+            _lib.check(rc, "evs_step_voxel")
 
         signal(0 if use_noise else _lib.EVS_VOXEL_FINALIZE)
         if not use_noise:
@@ -418,7 +432,7 @@ class EventSimulator:
         """accumulate_events_to_image (model.py:249-262) of every stream's events
         of the last step with t in [t_end - window_us, t_end) (default t_end: the
         end of the step): int64 [S, H, W] on the device, one launch for all
-        streams (evs_step_histogram; the bucket path sums the output rows)."""
+        streams (evs_step_histogram)."""
         import ctypes
 
         import torch
@@ -432,14 +446,6 @@ class EventSimulator:
         L = _lib.load()
         rc = L.evs_step_histogram(ctypes.byref(e.params), ctypes.byref(e.bufs), e.workspace.data_ptr(),
                                   e.workspace.numel(), int(window_us), t_end, out.data_ptr(), _lib.stream_ptr())
-        if rc == _lib.EVS_ERR_UNSUPPORTED:
-            from .represent import accumulate
-            from .events.types import concat_batches
-
-            for s in range(self.S):
-                b = concat_batches([self.segment(s, f) for f in range(self.T)])
-                out[s] = accumulate(b, int(window_us), t_end, self.W, self.H, device_output=True)
-            return out
         _lib.check(rc, "evs_step_histogram")
         return out
 

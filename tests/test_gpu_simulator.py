@@ -157,10 +157,10 @@ def test_run_host_pipeline_matches_oracle():
                 assert got[w][s][f].same_events(ob), (w, s, f)
 
 
-@pytest.mark.parametrize("noise_cap,path,canonical", [
-    (None, "tile", True), (8, "tile", True),   # 8: every noise buffer overflows -> retrying path
-    (None, "tile", False), (None, "bucket", True)])
-def test_voxel_window_signal_plus_noise_matches_oracle(noise_cap, path, canonical, monkeypatch):
+@pytest.mark.parametrize("noise_cap,canonical", [
+    (None, True), (8, True),   # 8: every noise buffer overflows -> retrying path
+    (None, False)])
+def test_voxel_window_signal_plus_noise_matches_oracle(noise_cap, canonical):
     """EventSimulator.voxel_window: the T frames' signal events plus per-frame
     exact noise of one window, accumulated without sorting / merging, equals
     the oracle's voxel grid of the concatenated window batch."""
@@ -168,8 +168,6 @@ def test_voxel_window_signal_plus_noise_matches_oracle(noise_cap, path, canonica
 
     from paper_2602_15018_b200.simulator import EventSimulator, mix64
 
-    if path == "bucket":
-        monkeypatch.setenv("EVS_PATH", "bucket")
     S, T, W, H = 2, 4, 160, 96
     cfg = ev.EventCameraConfig(c_pos=0.05, c_neg=0.05, refractory_us=0, noise_rate_hz=2000.0)
     sim = EventSimulator(W, H, streams=S, frames_per_step=T, config=cfg, canonical=canonical)
@@ -216,16 +214,13 @@ def test_voxel_window_wide_window_64bit_bins():
     np.testing.assert_array_equal(sim.voxel_window(0, bins=5).cpu().numpy(), exp)
 
 
-@pytest.mark.parametrize("path", ["tile", "bucket"])
-def test_histograms_all_streams_match_oracle(path, monkeypatch):
+def test_histograms_all_streams_match_oracle():
     """EventSimulator.histograms: accumulate_events_to_image of every stream in
     one launch, windows inside and across the step's frames."""
     import torch
 
     from paper_2602_15018_b200.simulator import EventSimulator
 
-    if path == "bucket":
-        monkeypatch.setenv("EVS_PATH", "bucket")
     S, T, W, H = 5, 3, 346, 260
     cfg = ev.EventCameraConfig(c_pos=0.2, c_neg=0.2, refractory_us=0)
     sim = EventSimulator(W, H, streams=S, frames_per_step=T, config=cfg)
