@@ -231,16 +231,89 @@ def measure_t1(args, dev, cfg, phase0, rank, order=None):
 
 
 def device_texture_ring(width, height, frames, drift, phase0, dev):
-    """_texture_frame (events_bench.py:19-26) evaluated on the GPU in f64 (bench input only)."""
+    """Ring of `frames` frames on the device, frame k = _texture_frame(phase0 + (k mod 50) * drift)
+    (events_bench.py:19-26, computed on the host in f64 like the reference, uploaded once)."""
     import torch
 
-    x = torch.arange(width, dtype=torch.float64, device=dev) / width
-    y = torch.arange(height, dtype=torch.float64, device=dev) / height
-    grid = y[:, None] * 2.0 + x[None, :] * 3.0
+    from paper_2602_15018_b200.synth import PERIOD_FRAMES, texture_frame
+
+    base = [torch.from_numpy(texture_frame(width, height, phase0 + k * drift)).to(dev)
+            for k in range(min(frames, PERIOD_FRAMES))]
     out = torch.empty((frames, height, width), dtype=torch.float32, device=dev)
     for k in range(frames):
-        out[k] = (0.5 + 0.45 * torch.sin(2.0 * math.pi * (grid + (phase0 + k * drift)))).to(torch.float32)
+        out[k].copy_(base[k % PERIOD_FRAMES])
     return out
+
+
+FIXTURE = os.path.join(ROOT, "tests", "golden", "bench_hd_t50.json")
+
+
+def _sha1(arrays) -> str:
+    import hashlib
+
+    h = hashlib.sha1()
+    for a, dt in zip(arrays, (np.uint64, np.uint16, np.uint16, np.int8)):
+        h.update(np.ascontiguousarray(np.asarray(a).astype(dt, copy=False)).tobytes())
+    return h.hexdigest()
+
+
+def verify_launch_shape(dev, T: int, frames: int = 150):
+    """Self-check of the benchmarked launch shape (HD, T frames per evs_step,
+    capacity 8P, fused validation, CUDA-graph replay with the device clock)
+    against the oracle fixture tests/golden/bench_hd_t50.json (per-frame
+    counts, drops, reservations, SHA-1 of the canonical events; the state).
+    The first step runs eagerly, the following ones as graph replays, exactly
+    like the timed region.  Returns the list of mismatching frames."""
+    import torch
+
+    from paper_2602_15018_b200 import _lib
+    from paper_2602_15018_b200 import events as ev
+    from paper_2602_15018_b200.runtime import StepEngine, StepShape
+    from paper_2602_15018_b200.synth import PERIOD_FRAMES, texture_frame
+
+    with open(FIXTURE) as f:
+        fx = json.load(f)
+    frames = min(frames, len(fx["frames"]))
+    P = W * H
+    cfg = ev.EventCameraConfig(c_pos=C_TH, c_neg=C_TH, refractory_us=REFR)
+    ring_len = T * PERIOD_FRAMES // math.gcd(T, PERIOD_FRAMES)
+    ring = device_texture_ring(W, H, ring_len, DRIFT, 0.0, dev)
+    st = ev.init_pixel_states(ev.IntensityFrame(W, H, 0, texture_frame(W, H, 0.0)), cfg, seed=0)
+    eng = StepEngine(StepShape(1, T, H, W, 8 * P, _lib.EVS_ORDER_CANONICAL, TICK, cfg.log_eps, REFR,
+                               st.uniform_thresholds), dev)
+    nsteps = (frames + T - 1) // T
+    bad = []
+    for i in range(nsteps):
+        win = ring[(i * T) % ring_len:(i * T) % ring_len + T]
+        if i == 0:
+            eng.launch(win, st.d_ref_log, st.d_last_event_t, t0=0, tick=TICK, validate=True)
+        else:
+            if i == 1 or (T % PERIOD_FRAMES):  # (windows repeat when T is a multiple of the period)
+                eng.capture([win], st.d_ref_log, st.d_last_event_t, tick=TICK, t0=i * T * TICK)
+            eng.replay()
+        torch.cuda.synchronize()
+        counts, dropped, res, badpx = eng.fetch_info()
+        if badpx != _lib.NO_BAD:
+            return ["invalid frame"]
+        for f in range(T):
+            j = i * T + f
+            if j >= frames:
+                break
+            n = int(counts[f])
+            got = {"count": n, "dropped": int(dropped[f]), "reservations": int(res[f]),
+                   "sha1": _sha1([eng.ev_t[f, :n].cpu().numpy(), eng.ev_x[f, :n].cpu().numpy(),
+                                  eng.ev_y[f, :n].cpu().numpy(), eng.ev_p[f, :n].cpu().numpy()])}
+            if got != fx["frames"][j]:
+                bad.append(j)
+    if nsteps * T == frames == len(fx["frames"]):
+        import hashlib
+
+        h = hashlib.sha1()
+        h.update(st.d_ref_log.cpu().numpy().tobytes())
+        h.update(st.d_last_event_t.cpu().numpy().tobytes())
+        if h.hexdigest() != fx["state_sha1"]:
+            bad.append("state")
+    return bad
 
 
 def run_ours(args):
@@ -415,6 +488,13 @@ def run_ours(args):
     gen_bytes = 4 * P * T + 4 * P + 20 * A + 8 * E_step  # K1's own traffic model (keys scratch)
     gen_achieved = gen_bytes / (stage_ms[1] / 1e3) / 1e9
 
+    # self-check of the timed launch shape against the oracle fixture (untimed)
+    mism = verify_launch_shape(dev, T)
+    self_check = {"fixture": "tests/golden/bench_hd_t50.json (oracle, 150 HD frames: per-frame counts, drops, "
+                             "reservations, SHA-1 of the canonical events; final state)",
+                  "launch": f"same StepShape (T={T}), eager step then CUDA-graph replays", "frames": 150,
+                  "mismatches": [str(m) for m in mism[:10]], "ok": not mism}
+
     per_frame = None
     if T != 1 and args.compare_t1:
         from paper_2602_15018_b200 import _lib
@@ -453,8 +533,13 @@ def run_ours(args):
         "e2e_per_frame_api": e2e_frame,
         "gpu_launches": K * 5 + reps,  # five kernels per evs_step (+ one clock init per graph replay)
         "clocks": clocks,
+        "self_check": self_check,
     }
     print(json.dumps(line), flush=True)
+    if not self_check["ok"]:
+        print(f"bench self-check FAILED: frames {self_check['mismatches']} differ from the oracle fixture",
+              file=sys.stderr)
+        sys.exit(1)
     if world > 1:
         dist.destroy_process_group()
 

@@ -4,6 +4,7 @@ CPU-only: pins the oracle before it is trusted as the checker of the CUDA path.
 """
 
 import os
+import sys
 
 import numpy as np
 import pytest
@@ -92,3 +93,28 @@ def test_oracle_voxel_definition(oracle_mod):
     v = oracle_mod.voxel(b, 0, 100, 5, 1, 1)[:, 0, 0]
     # t=0 -> tau=0 -> bin0 weight 1 ; t=50 -> tau=2 (bins of 25us) -> bin2 weight -1
     np.testing.assert_array_equal(v, np.array([1.0, 0.0, -1.0, 0.0, 0.0], np.float32))
+
+
+def test_bench_fixture_first_frames_from_oracle(oracle_mod):
+    """tests/golden/bench_hd_t50.json (bench.py's self-check fixture) is the
+    oracle's output: its first frames recomputed here (CPU)."""
+    import json
+    import os
+
+    from paper_2602_15018_b200.synth import texture_frame
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    sys.path.insert(0, here)
+    from make_bench_golden import batch_sha1
+
+    with open(os.path.join(here, "bench_hd_t50.json")) as f:
+        fx = json.load(f)
+    W, H = 1280, 720
+    oracle = oracle_mod
+    st = oracle.init_state(texture_frame(W, H, 0.0), c_pos=0.15, c_neg=0.15, refractory_us=100, seed=0)
+    for j in range(4):
+        b = oracle.canonical_sort(oracle.generate(st, texture_frame(W, H, 0.02 * j), j * 1000, (j + 1) * 1000,
+                                                  refractory_us=100))
+        assert fx["frames"][j] == {"count": len(b), "dropped": b.dropped_count,
+                                   "reservations": b.reservation_count,
+                                   "sha1": batch_sha1(b.t, b.x, b.y, b.polarity)}, j
