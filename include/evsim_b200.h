@@ -128,6 +128,14 @@ size_t evs_sort_workspace_bytes(int64_t n, int64_t t_span);
 evs_status evs_canonical_sort(int64_t n, int64_t* t, uint16_t* x, uint16_t* y, int8_t* p,
                               int64_t t_min, int64_t t_span, uint32_t epoch, void* workspace,
                               size_t workspace_bytes, void* stream);
+/* canonical_sort (parallel.py:112-123) of ANY device batch of n < 2^32 events,
+ * in place: t compared as uint64 (any span, values >= 2^63 included), any
+ * int8 polarity (signed order), stable.  Four LSD passes over 32-bit digits
+ * (polarity, (y, x), t low word, t high word), each a radix sort of 64-bit
+ * keys digit << 32 | position.  Workspace from evs_sort_general_workspace_bytes. */
+size_t evs_sort_general_workspace_bytes(int64_t n);
+evs_status evs_canonical_sort_general(int64_t n, int64_t* t, uint16_t* x, uint16_t* y, int8_t* p,
+                                      void* workspace, size_t workspace_bytes, void* stream);
 /* Stable merge of two canonical-ordered device batches A (signal) and B
  * (noise) into out[na + nb]: the canonical order of concat_batches([A, B])
  * (types.py:82-92 then parallel.py:112-123) without a full sort.  Requires
@@ -223,8 +231,7 @@ evs_status evs_step_voxel(const evs_step_params* p, const evs_step_buffers* b, c
 /* accumulate_events_to_image (model.py:249-262) of EVERY stream of the last
  * evs_step call on this workspace: out[s][y][x] (int64, device) = sum of the
  * polarities of stream s's events with t in [t_end - window_us, t_end), read
- * from the step's per-tile regions in one launch (tile-order path;
- * EVS_ERR_UNSUPPORTED after the bucket path). */
+ * from the step's per-tile regions in one launch. */
 evs_status evs_step_histogram(const evs_step_params* p, const evs_step_buffers* b, const void* workspace,
                               size_t workspace_bytes, int64_t window_us, int64_t t_end, int64_t* out,
                               void* stream);
@@ -237,6 +244,31 @@ evs_status evs_compact_segments(int32_t nseg, const int64_t* counts, int64_t seg
                                 const uint16_t* x, const uint16_t* y, const int8_t* p, int64_t* out_t,
                                 uint16_t* out_x, uint16_t* out_y, int8_t* out_p, int64_t out_capacity,
                                 void* stream);
+
+/* Stable k-way merge of nruns <= 64 sorted runs of int64 keys stored back to
+ * back in keys_in (run r = [run_offsets[r], run_offsets[r+1]), device int64)
+ * into keys_out (ties keep run order).  The row bands of one sensor
+ * are such runs of packed 8-byte keys whose integer order is
+ * the canonical order (parallel.py:112-123): their merge is the sensor's
+ * canonical batch. */
+evs_status evs_merge_runs(int32_t nruns, const int64_t* run_offsets, int64_t n, const int64_t* keys_in,
+                          int64_t* keys_out, void* stream);
+
+/* Packed event keys of an evs_step output for a gather to one rank (SURVEY.md
+ * 8(e); BASELINE config 5): the first counts[g] events of every segment
+ * g < nseg (stride seg_stride) back to back, segment order, as
+ *   key = (t - t_base) << (ybits + xbits + 1) | (y + y_offset) << (xbits + 1) | x << 1 | (p > 0)
+ * in 4 bytes (key_bytes = 4: the key must fit 31 bits, e.g. DAVIS 12+9+9+1)
+ * or 8 bytes (key_bytes = 8: t - t_base < 2^30, ybits = xbits = 16).  Integer
+ * order of the keys within a segment is the canonical (t, y, x, p) order.
+ * seg_offsets (device int64, nseg + 1) receives the exclusive prefix of the
+ * counts and the total; nothing is written at or beyond out_capacity keys.
+ * Replaces the host-side packing a consumer of parallel.py:112-123 output
+ * would do before a transfer.  y_offset shifts a row band's rows to sensor rows. */
+evs_status evs_pack_segments(int32_t nseg, const int64_t* counts, int64_t seg_stride, const int64_t* t,
+                             const uint16_t* x, const uint16_t* y, const int8_t* p, int64_t t_base,
+                             int32_t y_offset, int32_t key_bytes, int32_t ybits, int32_t xbits, void* out_keys,
+                             int64_t* seg_offsets, int64_t out_capacity, void* stream);
 
 /* limit_bandwidth (model.py:215-246) of a t-sorted device batch of n >= 1
  * events: keeps the first `cap` = int(rate * window * 1e-6) events of each
@@ -252,6 +284,13 @@ evs_status evs_limit_bandwidth(int64_t n, const int64_t* t, const uint16_t* x, c
  * out_fast[i] = the log used by evs_step, out_cuda[i] = CUDA's log(x[i]). */
 evs_status evs_selftest_log(int64_t n, const double* x, double* out_fast, double* out_cuda,
                             void* stream);
+
+/* log_transform (model.py:28-39) of n float32 intensities: out = log(double(v)
+ * + log_eps) (f64, <= 1 ulp) and, in the same pass, the first invalid value
+ * (not finite or outside [0, 1]) as a flat index in *bad_index (device int64,
+ * the caller initialises it to INT64_MAX; atomicMin). */
+evs_status evs_log_transform(int64_t n, const float* values, double log_eps, double* out, int64_t* bad_index,
+                             void* stream);
 
 /* numpy SeedSequence(seed) -> PCG64 state (host function, no GPU).
  * words: little-endian u32 words of the non-negative seed.

@@ -28,10 +28,11 @@ NO_BAD = 0x7FFFFFFFFFFFFFFF
 EXPORTED_SYMBOLS = (
     "evs_version", "evs_error_string", "evs_step_workspace_bytes", "evs_step",
     "evs_step_profiled", "evs_step_clock_init",
-    "evs_sort_workspace_bytes", "evs_canonical_sort", "evs_batch_stats", "evs_seed_pcg64",
+    "evs_sort_workspace_bytes", "evs_canonical_sort", "evs_sort_general_workspace_bytes",
+    "evs_canonical_sort_general", "evs_batch_stats", "evs_seed_pcg64",
     "evs_noise_workspace_bytes", "evs_noise", "evs_noise_batch_workspace_bytes", "evs_noise_batch",
     "evs_accumulate", "evs_voxel", "evs_voxel_segments", "evs_step_voxel", "evs_step_histogram",
-    "evs_compact_segments",
+    "evs_compact_segments", "evs_pack_segments", "evs_merge_runs", "evs_log_transform",
     "evs_limit_bandwidth_workspace_bytes", "evs_limit_bandwidth", "evs_render",
 )
 
@@ -123,6 +124,9 @@ def load():
         L.evs_sort_workspace_bytes.restype = sz
         L.evs_sort_workspace_bytes.argtypes = [i64, i64]
         L.evs_canonical_sort.argtypes = [i64, P, P, P, P, i64, i64, u32, P, sz, P]
+        L.evs_sort_general_workspace_bytes.restype = sz
+        L.evs_sort_general_workspace_bytes.argtypes = [i64]
+        L.evs_canonical_sort_general.argtypes = [i64, P, P, P, P, P, sz, P]
         L.evs_batch_stats.argtypes = [i64, P, P, P, P, P, P]
         L.evs_seed_pcg64.argtypes = [P, ctypes.c_int32, P]
         L.evs_seed_pcg64.restype = None
@@ -153,6 +157,9 @@ def _bind_extras(L) -> None:
     L.evs_step_voxel.argtypes = [P, P, P, sz, i32, i64, i64, i32, i32, P, P, sz, P]
     L.evs_step_histogram.argtypes = [P, P, P, sz, i64, i64, P, P]
     L.evs_compact_segments.argtypes = [i32, P, i64, P, P, P, P, P, P, P, P, i64, P]
+    L.evs_pack_segments.argtypes = [i32, P, i64, P, P, P, P, i64, i32, i32, i32, i32, P, P, i64, P]
+    L.evs_merge_runs.argtypes = [i32, P, i64, P, P, P]
+    L.evs_log_transform.argtypes = [i64, P, ctypes.c_double, P, P, P]
     L.evs_limit_bandwidth_workspace_bytes.restype = sz
     L.evs_limit_bandwidth_workspace_bytes.argtypes = [i64]
     L.evs_limit_bandwidth.argtypes = [i64, P, P, P, P, i64, i64, P, P, P, P, P, P, sz, P]

@@ -8,7 +8,8 @@ on that slice, canonical order, y shifted to sensor rows).  The only
 exchanges are per frame an all_gather of five int64 per band (events
 generated, events kept, reservations, first invalid pixel, its value) and,
 where a consumer needs the frame on one rank, ``gather_keys`` of the packed
-8-byte keys (``distributed.py``).
+8-byte keys (``distributed.py``; written by the evs_pack_segments kernel) and
+one k-way merge of the bands' sorted runs on that rank (evs_merge_runs).
 
 The result equals the unsplit reference (model.py:79-171, parallel.py:126-273
 followed by canonical_sort, parallel.py:112-123):
@@ -114,19 +115,27 @@ def bad_pixel_error(flat: int, bits: int, width: int) -> ValueError:
     return ValueError(f"invalid intensity {val!r} at pixel (x={xx}, y={yy})")
 
 
-def merge_keys(keys):
-    """Sensor order from the bands' sorted keys (key order is canonical)."""
+def merge_keys(keys, counts):
+    """Sensor order from the bands' sorted key runs (band order, ``counts``
+    keys each): the evs_merge_runs kernel (key order is canonical, and a
+    band's rows all precede the next band's, so this is SURVEY.md 8(e)'s
+    (t, band) placement)."""
     import torch
 
-    if keys.numel() == 0:
+    if keys.numel() == 0 or len(counts) == 1:
         return keys
-    return torch.sort(keys, stable=True).values
+    offs = torch.tensor(np.concatenate([[0], np.cumsum(counts)]), dtype=torch.int64, device=keys.device)
+    out = torch.empty_like(keys)
+    rc = _lib.load().evs_merge_runs(len(counts), offs.data_ptr(), keys.numel(), keys.data_ptr(), out.data_ptr(),
+                                    _lib.stream_ptr())
+    _lib.check(rc, "evs_merge_runs")
+    return out
 
 
 def keys_to_batch(keys, t_prev: int, dropped: int, device_output: bool = False):
-    from .distributed import unpack_keys
+    from .distributed import KEY64_LAYOUT, unpack_keys
 
-    t, x, y, p = unpack_keys(keys, int(t_prev))
+    t, x, y, p = unpack_keys(keys, int(t_prev), KEY64_LAYOUT)
     if device_output:
         return DeviceEventBatch(t, x.short(), y.short(), p, dropped_count=int(dropped),
                                 canonical=True)
@@ -207,7 +216,7 @@ class GpuBand:
         capacity; keep=k: pixel-major order, the first k events (then sorted)."""
         import torch
 
-        from .distributed import pack_keys
+        from .distributed import KEY64_LAYOUT, pack_segments
         from .represent import canonical_sort
 
         if self.height == 0:
@@ -229,12 +238,15 @@ class GpuBand:
         total = n + int(dropped[0])
         if keep is not None:
             n = min(n, int(keep))
-        b = DeviceEventBatch(eng.ev_t[0, :n], eng.ev_x[0, :n], eng.ev_y[0, :n], eng.ev_p[0, :n])
-        if keep is not None and n > 0:
-            b = canonical_sort(b)
-        y = b.y.to(torch.int64) & 0xFFFF
-        keys = pack_keys(b.t, b.x.to(torch.int64) & 0xFFFF, y + self.y0, b.polarity, int(t_prev))
-        return BandResult(total, n, int(res[0]), NO_BAD, 0, keys)
+        rows = (eng.ev_t, eng.ev_x, eng.ev_y, eng.ev_p)
+        cnt = eng.info[0, :1]
+        if keep is not None and n > 0:  # the first `keep` pixel-major events, then canonical order
+            b = canonical_sort(DeviceEventBatch(eng.ev_t[0, :n], eng.ev_x[0, :n], eng.ev_y[0, :n], eng.ev_p[0, :n]))
+            rows = (b.t[None], b.x[None], b.y[None], b.polarity[None])
+            cnt = torch.tensor([n], dtype=torch.int64, device=self.device)
+        # 8-byte keys (t - t_prev) << 33 | sensor row << 17 | x << 1 | p, written by the evs_pack_segments kernel
+        keys, _ = pack_segments(cnt, rows, int(t_prev), KEY64_LAYOUT, 8, y_offset=self.y0)
+        return BandResult(total, n, int(res[0]), NO_BAD, 0, keys[:n])
 
 
 class TorchComm:
@@ -258,10 +270,10 @@ class TorchComm:
         return [[int(v) for v in o.tolist()] for o in out]
 
     def gather_keys(self, keys, dst: int):
+        """(keys of every band back to back in band order, per-band counts) on dst."""
         from .distributed import gather_keys
 
-        out, _ = gather_keys(keys.contiguous(), dst=dst, group=self.group)
-        return out
+        return gather_keys(keys.contiguous(), dst=dst, group=self.group)
 
 
 class BandedCamera:
@@ -271,10 +283,12 @@ class BandedCamera:
     other ranks, or on every rank with gather=False) and fills ``stats``
     (reservation_count, events_emitted) like generate_events_parallel."""
 
-    def __init__(self, band, comm, config: EventCameraConfig, sensor_width: int, sensor_height: int):
+    def __init__(self, band, comm, config: EventCameraConfig, sensor_width: int, sensor_height: int,
+                 merge=merge_keys):
         self.band, self.comm, self.config = band, comm, config
         self.width, self.height = int(sensor_width), int(sensor_height)
         self.cap = int(config.capacity(self.width, self.height))
+        self.merge = merge  # (keys, per-band counts) -> merged keys (the kernel; CPU tests pass a stand-in)
 
     def step(self, frame, t_prev: int, t_now: int, stats=None, dst: int = 0, gather: bool = True,
              device_output: bool = False):
@@ -299,10 +313,10 @@ class BandedCamera:
             stats.events_emitted = plan.written
         if not gather:
             return None
-        keys = self.comm.gather_keys(r.keys, dst)
+        keys, counts = self.comm.gather_keys(r.keys, dst)
         if me != dst:
             return None
-        return keys_to_batch(merge_keys(keys), t_prev, plan.dropped, device_output)
+        return keys_to_batch(self.merge(keys, counts), t_prev, plan.dropped, device_output)
 
 
 class LocalBands:
@@ -334,4 +348,5 @@ class LocalBands:
             stats.reservation_count = plan.reservations
             stats.events_emitted = plan.written
         keys = torch.cat([r.keys.to(res[0].keys.device) for r in res])
-        return keys_to_batch(merge_keys(keys), t_prev, plan.dropped, device_output)
+        return keys_to_batch(merge_keys(keys, [int(r.keys.numel()) for r in res]), t_prev, plan.dropped,
+                             device_output)

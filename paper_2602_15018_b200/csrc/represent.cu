@@ -294,6 +294,50 @@ __global__ void __launch_bounds__(256) k_compact_segments(const int64_t* __restr
   }
 }
 
+// ---- log_transform (model.py:28-39) -----------------------------------------
+__global__ void __launch_bounds__(256) k_log_transform(int64_t n, const float* __restrict__ v, double eps,
+                                                       double* __restrict__ out, int64_t* bad) {
+  int64_t first = kNoBad;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float x = v[i];
+    if (!(x >= 0.f && x <= 1.f)) first = min(first, i);  // NaN / inf / out of range (model.py:33-38)
+    out[i] = log((double)x + eps);                          // model.py:39, f64
+  }
+  for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+  if ((threadIdx.x & 31) == 0 && first != kNoBad)
+    atomicMin(reinterpret_cast<unsigned long long*>(bad), (unsigned long long)first);
+}
+
+// ---- packed keys of a step's segments (gather payload) ---------------------
+template <typename K>
+__global__ void __launch_bounds__(256) k_pack_segments(const int64_t* __restrict__ counts, int64_t seg_stride,
+                                                       const int64_t* __restrict__ t, const uint16_t* __restrict__ x,
+                                                       const uint16_t* __restrict__ y, const int8_t* __restrict__ p,
+                                                       int64_t t_base, int y_off, int ysh, int xsh, K* out,
+                                                       int64_t* offs, int64_t out_cap) {
+  __shared__ int64_t s_pre[9];
+  const int g = blockIdx.y, tid = threadIdx.x;
+  int64_t part = 0;
+  for (int j = tid; j < g; j += blockDim.x) part += counts[j];
+  int64_t tot;
+  block_excl_scan<256, int64_t>(part, s_pre, &tot);
+  const int64_t pre = tot;
+  int64_t n = counts[g];
+  if (blockIdx.x == 0 && tid == 0) {
+    offs[g] = pre;
+    if (g == gridDim.y - 1) offs[g + 1] = pre + n;
+  }
+  if (pre + n > out_cap) n = out_cap - pre;
+  const int64_t src = (int64_t)g * seg_stride;
+  const int tsh = ysh + xsh + 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + tid; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t tr = (uint64_t)(__ldcs(t + src + i) - t_base);
+    const uint64_t k = (tr << tsh) | ((uint64_t)(__ldcs(y + src + i) + y_off) << (xsh + 1)) |
+                       ((uint64_t)__ldcs(x + src + i) << 1) | (__ldcs(p + src + i) > 0 ? 1u : 0u);
+    out[pre + i] = (K)k;
+  }
+}
+
 // ---- limit_bandwidth -------------------------------------------------------
 // keep[i] = rank of i in its window < cap; per-block kept counts; unsorted flag
 __global__ void __launch_bounds__(1024) k_lb_flags(int64_t n, const int64_t* __restrict__ t, int64_t window,
@@ -430,6 +474,38 @@ evs_status evs_compact_segments(int32_t nseg, const int64_t* counts, int64_t seg
   const int bx = (148 * 8 + nseg - 1) / nseg;
   k_compact_segments<<<dim3(bx < 2 ? 2 : bx, nseg), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       counts, seg_stride, t, x, y, p, out_t, out_x, out_y, out_p, out_capacity);
+  return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
+}
+
+evs_status evs_log_transform(int64_t n, const float* values, double log_eps, double* out, int64_t* bad_index,
+                             void* stream) {
+  if (n < 0 || !(log_eps > 0) || !bad_index) return EVS_ERR_ARG;
+  if (n == 0) return EVS_OK;
+  if (!values || !out) return EVS_ERR_ARG;
+  k_log_transform<<<grid_for(n, 148 * 16), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, values, log_eps, out,
+                                                                                        bad_index);
+  return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
+}
+
+evs_status evs_pack_segments(int32_t nseg, const int64_t* counts, int64_t seg_stride, const int64_t* t,
+                             const uint16_t* x, const uint16_t* y, const int8_t* p, int64_t t_base,
+                             int32_t y_offset, int32_t key_bytes, int32_t ybits, int32_t xbits, void* out_keys,
+                             int64_t* seg_offsets, int64_t out_capacity, void* stream) {
+  if (nseg < 1 || nseg > 65535 || seg_stride < 0 || out_capacity < 0) return EVS_ERR_ARG;
+  if (!counts || !t || !x || !y || !p || !out_keys || !seg_offsets) return EVS_ERR_ARG;
+  if (ybits < 1 || xbits < 1 || ybits > 16 || xbits > 16 || y_offset < 0) return EVS_ERR_ARG;
+  if (key_bytes == 8 && (ybits != 16 || xbits != 16)) return EVS_ERR_ARG;
+  const int bx = (148 * 8 + nseg - 1) / nseg;
+  const dim3 grid(bx < 2 ? 2 : bx, nseg);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (key_bytes == 4)
+    k_pack_segments<uint32_t><<<grid, 256, 0, st>>>(counts, seg_stride, t, x, y, p, t_base, y_offset, ybits, xbits,
+                                                   static_cast<uint32_t*>(out_keys), seg_offsets, out_capacity);
+  else if (key_bytes == 8)
+    k_pack_segments<uint64_t><<<grid, 256, 0, st>>>(counts, seg_stride, t, x, y, p, t_base, y_offset, ybits, xbits,
+                                                   static_cast<uint64_t*>(out_keys), seg_offsets, out_capacity);
+  else
+    return EVS_ERR_ARG;
   return cudaGetLastError() == cudaSuccess ? EVS_OK : EVS_ERR_CUDA;
 }
 

@@ -5,9 +5,10 @@ independent), so scaling is by sharding streams across ranks.  NCCL is used
 only when a consumer needs the events on one rank (BASELINE configs[4]):
 ``gather_keys`` is a gatherv built from an all_gather of the per-rank counts
 (8 bytes per rank) plus grouped point-to-point sends into prefix offsets on
-the destination (NCCL has no gatherv).  Events travel as the packed 64-bit
-keys the kernels already use (t_rel << 33 | y << 17 | x << 1 | p), 8 bytes
-per event instead of the 13-byte SoA.
+the destination (NCCL has no gatherv).  Events travel as packed keys written
+on the device by the evs_pack_segments kernel: 4 bytes per event when the
+sensor and the time span fit 31 bits (DAVIS: t_rel 12 + y 9 + x 9 + p 1),
+else 8 (t_rel < 2^30 | y | x | p), instead of the 13-byte SoA.
 """
 
 from __future__ import annotations
@@ -21,21 +22,6 @@ def shard_streams(num_streams: int, world_size: int, rank: int) -> list[int]:
     return [s for s in range(num_streams) if (s * world_size) // num_streams == rank]
 
 
-def pack_keys(t: torch.Tensor, x: torch.Tensor, y: torch.Tensor, p: torch.Tensor, t_base: int) -> torch.Tensor:
-    """SoA events -> packed int64 keys relative to t_base (t - t_base < 2**31)."""
-    tr = (t - t_base).to(torch.int64)
-    return (tr << 33) | ((y.to(torch.int64) & 0xFFFF) << 17) | ((x.to(torch.int64) & 0xFFFF) << 1) | \
-        (p > 0).to(torch.int64)
-
-
-def unpack_keys(k: torch.Tensor, t_base: int):
-    t = (k >> 33) + t_base
-    y = ((k >> 17) & 0xFFFF).to(torch.int32)
-    x = ((k >> 1) & 0xFFFF).to(torch.int32)
-    p = torch.where((k & 1) == 1, 1, -1).to(torch.int8)
-    return t, x, y, p
-
-
 def key32_layout(width: int, height: int, span_us: int):
     """Bit widths (t_rel, y, x) of a 4-byte key t_rel << (yb + xb + 1) | y << (xb + 1)
     | x << 1 | p for a sensor and a time span (DAVIS events in
@@ -47,17 +33,33 @@ def key32_layout(width: int, height: int, span_us: int):
     return (tb, yb, xb) if tb + yb + xb + 1 <= 31 else None
 
 
-def pack_keys32(t: torch.Tensor, x: torch.Tensor, y: torch.Tensor, p: torch.Tensor, t_base: int,
-                layout) -> torch.Tensor:
-    """SoA events -> int32 keys (layout from key32_layout; 0 <= t - t_base < 2**tb)."""
-    tb, yb, xb = layout
-    tr = (t - t_base).to(torch.int64)
-    k = (tr << (yb + xb + 1)) | ((y.to(torch.int64) & 0xFFFF) << (xb + 1)) | \
-        ((x.to(torch.int64) & 0xFFFF) << 1) | (p > 0).to(torch.int64)
-    return k.to(torch.int32)
+KEY64_LAYOUT = (30, 16, 16)  # 8-byte keys: t_rel < 2^30 (the sign bit stays clear), 16-bit y and x
 
 
-def unpack_keys32(k: torch.Tensor, t_base: int, layout):
+def pack_segments(counts, rows, t_base: int, layout, key_bytes: int, out=None, y_offset: int = 0):
+    """Packed keys of an evs_step output (device [nseg][cap] SoA rows t, x, y, p
+    and device per-segment counts) written back to back by the evs_pack_segments
+    kernel.  Returns (keys, offsets[nseg + 1]) on the device, no host sync;
+    ``out`` (a big enough 1-D int32 / int64 tensor) is reused when given;
+    ``y_offset`` shifts a row band's rows to sensor rows."""
+    from . import _lib
+
+    t, x, y, p = rows
+    nseg, cap = t.shape
+    dt = torch.int32 if key_bytes == 4 else torch.int64
+    if out is None or out.dtype != dt or out.numel() < nseg * cap:
+        out = torch.empty(nseg * cap, dtype=dt, device=t.device)
+    offs = torch.empty(nseg + 1, dtype=torch.int64, device=t.device)
+    _, yb, xb = layout
+    rc = _lib.load().evs_pack_segments(nseg, counts.data_ptr(), cap, t.data_ptr(), x.data_ptr(), y.data_ptr(),
+                                       p.data_ptr(), int(t_base), int(y_offset), key_bytes, yb, xb, out.data_ptr(),
+                                       offs.data_ptr(), out.numel(), _lib.stream_ptr())
+    _lib.check(rc, "evs_pack_segments")
+    return out, offs
+
+
+def unpack_keys(k: torch.Tensor, t_base: int, layout):
+    """Packed keys -> (t, x, y, p) tensors (consumer side; 4- or 8-byte keys)."""
     tb, yb, xb = layout
     k = k.to(torch.int64)
     t = (k >> (yb + xb + 1)) + t_base
@@ -67,19 +69,28 @@ def unpack_keys32(k: torch.Tensor, t_base: int, layout):
     return t, x, y, p
 
 
+def pack_keys(t, x, y, p, t_base: int, layout):
+    """SoA events -> packed keys with torch ops (tests and host-side callers; the
+    step output is packed on the device by pack_segments).  Raises when a time
+    does not fit the layout's t_rel bits."""
+    tb, yb, xb = layout
+    tr = (t.to(torch.int64) - t_base)
+    if tr.numel() and (int(tr.min()) < 0 or int(tr.max()) >= (1 << tb)):
+        raise ValueError(f"event times must lie in [t_base, t_base + 2**{tb})")
+    k = (tr << (yb + xb + 1)) | ((y.to(torch.int64) & 0xFFFF) << (xb + 1)) | \
+        ((x.to(torch.int64) & 0xFFFF) << 1) | (p > 0).to(torch.int64)
+    return k.to(torch.int32) if tb + yb + xb + 1 <= 31 else k
+
+
 def gather_events(t, x, y, p, t_base: int, width: int, height: int, span_us: int, dst: int = 0, group=None):
     """Gather every rank's events (SoA, times in [t_base, t_base + span_us)) to
     ``dst`` in rank order as packed keys: 4 bytes per event when the sensor and
     span fit in 31 bits (DAVIS: 12 + 9 + 9 + 1), else 8.  Returns (t, x, y, p)
     on dst, None elsewhere; the same layout decision on every rank."""
-    lay = key32_layout(width, height, span_us)
-    if lay is None:
-        keys = pack_keys(t, x, y, p, t_base)
-        out, _ = gather_keys(keys, dst=dst, group=group)
-        return None if out is None else unpack_keys(out, t_base)
-    keys = pack_keys32(t, x, y, p, t_base, lay)
+    lay = key32_layout(width, height, span_us) or KEY64_LAYOUT
+    keys = pack_keys(t, x, y, p, t_base, lay)
     out, _ = gather_keys(keys, dst=dst, group=group)
-    return None if out is None else unpack_keys32(out, t_base, lay)
+    return None if out is None else unpack_keys(out, t_base, lay)
 
 
 def gather_keys(local: torch.Tensor, dst: int = 0, group=None):

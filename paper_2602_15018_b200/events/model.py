@@ -40,7 +40,8 @@ def _bad_pixel_error(values, flat: int, width: int) -> ValueError:
 def log_transform(frame: IntensityFrame, log_eps: float) -> np.ndarray:
     """model.py:28-39: per-pixel ln(I + log_eps) in float64; validates the frame.
 
-    Computed on the GPU (f64 log); returned as a host array like the reference.
+    One pass of the evs_log_transform kernel (f64 log, <= 1 ulp; the first
+    invalid pixel by atomicMin); returned as a host array like the reference.
     """
     import torch
 
@@ -48,12 +49,17 @@ def log_transform(frame: IntensityFrame, log_eps: float) -> np.ndarray:
         raise ValueError("log_eps must be positive")
     _lib.require_cuda()
     v = frame.values
-    d = v if _is_torch(v) else torch.from_numpy(np.ascontiguousarray(v)).cuda()
-    bad = ~torch.isfinite(d) | (d < 0) | (d > 1)
-    if bool(bad.any()):
-        flat = int(torch.nonzero(bad.reshape(-1))[0].item())
+    d = (v if _is_torch(v) else torch.from_numpy(np.ascontiguousarray(v, np.float32))).cuda()
+    d = d.to(torch.float32).contiguous()
+    out = torch.empty(d.shape, dtype=torch.float64, device=d.device)
+    bad = torch.full((1,), _lib.NO_BAD, dtype=torch.int64, device=d.device)
+    rc = _lib.load().evs_log_transform(d.numel(), d.data_ptr(), float(log_eps), out.data_ptr(), bad.data_ptr(),
+                                       _lib.stream_ptr())
+    _lib.check(rc, "evs_log_transform")
+    flat = int(bad.item())
+    if flat != _lib.NO_BAD:
         raise _bad_pixel_error(v, flat, frame.width)
-    return torch.log(d.double() + log_eps).cpu().numpy()
+    return out.cpu().numpy()
 
 
 def init_pixel_states(frame0: IntensityFrame, config: EventCameraConfig, seed: int) -> PixelStateGrid:

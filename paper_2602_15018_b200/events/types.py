@@ -260,10 +260,18 @@ class PixelStateGrid:
                 self.uniform_thresholds = (float(hp[0]), float(hn[0]))
         self._ctx = {}
 
-    # reference attribute names -> host copies
+    # Reference attribute names -> READ-ONLY host snapshots of the HBM state (an
+    # in-place edit such as ``state.ref_log[mask] = v`` raises instead of being
+    # silently lost); assign the whole attribute to write: ``state.ref_log = a``.
+    @staticmethod
+    def _snapshot(t) -> np.ndarray:
+        a = t.cpu().numpy()
+        a.flags.writeable = False
+        return a
+
     @property
     def ref_log(self) -> np.ndarray:
-        return self.d_ref_log.cpu().numpy()
+        return self._snapshot(self.d_ref_log)
 
     @ref_log.setter
     def ref_log(self, v) -> None:
@@ -271,7 +279,7 @@ class PixelStateGrid:
 
     @property
     def last_event_t(self) -> np.ndarray:
-        return self.d_last_event_t.cpu().numpy()
+        return self._snapshot(self.d_last_event_t)
 
     @last_event_t.setter
     def last_event_t(self, v) -> None:
@@ -279,11 +287,30 @@ class PixelStateGrid:
 
     @property
     def thresholds_pos(self) -> np.ndarray:
-        return self.d_thresholds_pos.cpu().numpy()
+        return self._snapshot(self.d_thresholds_pos)
+
+    @thresholds_pos.setter
+    def thresholds_pos(self, v) -> None:
+        self.d_thresholds_pos.copy_(_as_tensor(v, self.d_thresholds_pos))
+        self._refresh_uniform()
 
     @property
     def thresholds_neg(self) -> np.ndarray:
-        return self.d_thresholds_neg.cpu().numpy()
+        return self._snapshot(self.d_thresholds_neg)
+
+    @thresholds_neg.setter
+    def thresholds_neg(self, v) -> None:
+        self.d_thresholds_neg.copy_(_as_tensor(v, self.d_thresholds_neg))
+        self._refresh_uniform()
+
+    def _refresh_uniform(self) -> None:
+        """Thresholds changed: constant grids let the kernels read one scalar."""
+        hp = self.d_thresholds_pos.reshape(-1)
+        hn = self.d_thresholds_neg.reshape(-1)
+        if hp.numel() and bool((hp == hp[0]).all()) and bool((hn == hn[0]).all()):
+            self.uniform_thresholds = (float(hp[0].item()), float(hn[0].item()))
+        else:
+            self.uniform_thresholds = None
 
     def copy(self) -> "PixelStateGrid":
         c = PixelStateGrid.__new__(PixelStateGrid)

@@ -80,19 +80,29 @@ def canonical_sort(batch):
         # concat_batches([signal (canonical), noise]): sort the small part, merge
         a, was_host = _device_batch(parts[0])
         b = canonical_sort(parts[1].to_device() if not isinstance(parts[1], DeviceEventBatch) else parts[1])
-        if len(a) and len(b) and batch_stats(a)[4] == 0 and batch_stats(b)[4] == 0:
+        sa = batch_stats(a) if len(a) else None
+        sb = batch_stats(b) if len(b) else None
+        if (sa and sb and sa[4] == 0 and sb[4] == 0 and min(sa[0], sb[0]) >= 0
+                and max(sa[1], sb[1]) - min(sa[0], sb[0]) < (1 << 31)):
             out = merge_canonical(a, b)
             return out.to_host() if not isinstance(batch, DeviceEventBatch) else out
     db, was_host = _device_batch(batch)
     n = len(db)
     tmin, tmax, _xm, _ym, badp = batch_stats(db)
     span = tmax - tmin
-    if badp or span >= (1 << 31) or tmin < 0:
-        raise NotImplementedError("canonical_sort on the GPU needs polarity in {-1,+1}, "
-                                  "0 <= t and max(t)-min(t) < 2**31")
     out = DeviceEventBatch(db.t.clone(), db.x.clone(), db.y.clone(), db.polarity.clone(),
                            dropped_count=db.dropped_count, canonical=True)
     L = _lib.load()
+    if badp or span >= (1 << 31) or tmin < 0:
+        # outside the simulator's range (polarity not +-1, uint64 times >= 2^63
+        # or spanning >= 2^31 us): the general four-pass sort
+        if n >= (1 << 32):
+            raise ValueError("canonical_sort on the GPU handles < 2**32 events per batch")
+        ws, _ep = _workspace(("sort_general", db.t.device), L.evs_sort_general_workspace_bytes(n), db.t.device)
+        rc = L.evs_canonical_sort_general(n, out.t.data_ptr(), out.x.data_ptr(), out.y.data_ptr(),
+                                          out.polarity.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+        _lib.check(rc, "evs_canonical_sort_general")
+        return out.to_host() if was_host else out
     nbytes = L.evs_sort_workspace_bytes(n, span)
     ws, ep = _workspace(("sort", db.t.device), nbytes, db.t.device)
     rc = L.evs_canonical_sort(n, out.t.data_ptr(), out.x.data_ptr(), out.y.data_ptr(),

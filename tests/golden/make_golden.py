@@ -151,8 +151,40 @@ def main() -> None:
     raw = np.random.PCG64(99).random_raw(64)
     np.savez_compressed(os.path.join(HERE, "pcg64.npz"), seeds=np.array(seeds, dtype=object).astype(str),
                         states=np.array(states, np.uint64), raw99=raw, ints99=draws)
+    sort_general()
     print("golden fixtures written to", HERE)
 
 
+def sort_general() -> None:
+    """canonical_sort (parallel.py:112-123) of a batch outside the simulator's
+    range: uint64 times spanning > 2^31 us and >= 2^63, any int8 polarity,
+    duplicate (t, y, x) with different polarities."""
+    sys.dont_write_bytecode = True
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    from evsim.events import canonical_sort
+    from evsim.events.types import EventBatch
+
+    rng = np.random.default_rng(321)
+    n = 20000
+    t = np.concatenate([rng.integers(0, 2**40, n // 4, dtype=np.uint64),
+                        rng.integers(2**63 - 50, 2**63 + 50, n // 4, dtype=np.uint64),
+                        rng.integers(0, 40, n // 4, dtype=np.uint64),
+                        rng.integers(2**64 - 2**33, 2**64 - 1, n - 3 * (n // 4), dtype=np.uint64,
+                                     endpoint=True)])
+    x = rng.integers(0, 7, n).astype(np.uint16)
+    y = rng.integers(0, 5, n).astype(np.uint16)
+    x[: n // 8] = rng.integers(0, 65536, n // 8)
+    p = rng.integers(-128, 128, n).astype(np.int8)
+    p[n // 2:] = (rng.integers(0, 2, n - n // 2) * 2 - 1)
+    b = EventBatch(t=t, x=x, y=y, polarity=p, dropped_count=9)
+    cs = canonical_sort(b)
+    np.savez_compressed(os.path.join(HERE, "sort_general.npz"), t=t.view(np.int64), x=x, y=y, p=p,
+                        cs_t=cs.t.view(np.int64), cs_x=cs.x, cs_y=cs.y, cs_p=cs.polarity)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["sort_general"]:
+        sort_general()
+    else:
+        main()

@@ -16,7 +16,7 @@ import torch.multiprocessing as mp
 import oracle
 from paper_2602_15018_b200.bands import (NO_BAD, BandedCamera, BandResult, TorchComm, band_rows,
                                          plan_frame)
-from paper_2602_15018_b200.distributed import pack_keys
+from paper_2602_15018_b200.distributed import KEY64_LAYOUT, pack_keys
 from paper_2602_15018_b200.events.parallel import AggregationStats
 from paper_2602_15018_b200.events.types import EventCameraConfig
 
@@ -60,8 +60,15 @@ class OracleBand:
         b = oracle.canonical_sort(b)
         keys = pack_keys(torch.from_numpy(b.t.astype(np.int64)), torch.from_numpy(b.x.astype(np.int64)),
                          torch.from_numpy(b.y.astype(np.int64)) + self.y0, torch.from_numpy(b.polarity),
-                         int(t_prev))
+                         int(t_prev), KEY64_LAYOUT)
         return BandResult(total if total is not None else len(b), len(b), b.reservation_count, NO_BAD, 0, keys)
+
+
+def host_merge(keys, counts):
+    """Test stand-in for the evs_merge_runs kernel (CPU tensors over gloo): a
+    stable sort of the bands' runs (key order is the canonical order)."""
+    assert sum(counts) == keys.numel()
+    return keys[np.argsort(keys.numpy(), kind="stable")]
 
 
 def test_band_rows_partition_and_alignment():
@@ -107,7 +114,7 @@ def _worker(rank, world, port, q, case):
         ref_full = full.copy()
         rows = band_rows(H, W, world)
         band = OracleBand(full, rows[rank], cfg)
-        cam = BandedCamera(band, TorchComm(), cfg, W, H)
+        cam = BandedCamera(band, TorchComm(), cfg, W, H, merge=host_merge)
         out = []
         for k in range(1, len(frames)):
             fr = frames[k].copy()

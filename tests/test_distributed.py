@@ -9,8 +9,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2602_15018_b200.distributed import (gather_events, gather_fixed, gather_keys, key32_layout, pack_keys,
-                                               pack_keys32, shard_streams, unpack_keys, unpack_keys32)
+from paper_2602_15018_b200.distributed import (KEY64_LAYOUT, gather_events, gather_fixed, gather_keys, key32_layout,
+                                               pack_keys, shard_streams, unpack_keys)
 
 
 def _free_port():
@@ -30,7 +30,7 @@ def _worker(rank, world, port, q):
         x = torch.full_like(t, rank + 1).to(torch.int16)
         y = torch.full_like(t, 7).to(torch.int16)
         p = torch.where(t % 2 == 0, 1, -1).to(torch.int8)
-        keys = pack_keys(t, x, y, p, 1000)
+        keys = pack_keys(t, x, y, p, 1000, KEY64_LAYOUT)
         out, counts = gather_keys(keys, dst=0)
         hist = torch.full((3, 4), rank, dtype=torch.int64)
         stacked = gather_fixed(hist, dst=0)
@@ -69,9 +69,14 @@ def test_pack_unpack_roundtrip():
     x = torch.tensor([0, 345, 1279], dtype=torch.int16)
     y = torch.tensor([0, 259, 719], dtype=torch.int16)
     p = torch.tensor([1, -1, 1], dtype=torch.int8)
-    t2, x2, y2, p2 = unpack_keys(pack_keys(t, x, y, p, 10**9), 10**9)
+    t2, x2, y2, p2 = unpack_keys(pack_keys(t, x, y, p, 10**9, KEY64_LAYOUT), 10**9, KEY64_LAYOUT)
     assert torch.equal(t2, t) and torch.equal(x2, x.to(torch.int32)) and torch.equal(y2, y.to(torch.int32))
     assert torch.equal(p2, p)
+    # 8-byte keys stay non-negative: t - t_base must be < 2^30 (ADVICE: no sign-bit overflow)
+    with pytest.raises(ValueError):
+        pack_keys(t + (1 << 30), x, y, p, 10**9, KEY64_LAYOUT)
+    with pytest.raises(ValueError):
+        pack_keys(t - 10, x, y, p, 10**9, KEY64_LAYOUT)
 
 
 @pytest.mark.timeout(120)
@@ -93,7 +98,7 @@ def test_gatherv_two_ranks_gloo():
         assert x == [v & 0xFFFF for v in x0 + x1] and y == [v & 0xFFFF for v in y0 + y1]
     assert counts == [4 * 1, 4 * 4]
     keys = torch.tensor(out)
-    t, x, y, p = unpack_keys(keys, 1000)
+    t, x, y, p = unpack_keys(keys, 1000, KEY64_LAYOUT)
     # rank order preserved: rank 0's events first
     assert x[:4].tolist() == [1] * 4 and x[4:].tolist() == [2] * 16
     assert t[:4].tolist() == [1000, 1001, 1002, 1003]
@@ -110,10 +115,11 @@ def test_key32_layout_roundtrip_and_order():
     x = torch.randint(0, 640, (n,), generator=g).to(torch.int16)
     y = torch.randint(0, 480, (n,), generator=g).to(torch.int16)
     p = (torch.randint(0, 2, (n,), generator=g) * 2 - 1).to(torch.int8)
-    k = pack_keys32(t, x, y, p, 10**9, lay)
+    k = pack_keys(t, x, y, p, 10**9, lay)
     assert k.dtype == torch.int32 and int(k.min()) >= 0
-    t2, x2, y2, p2 = unpack_keys32(k, 10**9, lay)
+    t2, x2, y2, p2 = unpack_keys(k, 10**9, lay)
     assert torch.equal(t2, t) and torch.equal(x2, x.to(torch.int32)) and torch.equal(y2, y.to(torch.int32))
     assert torch.equal(p2, p)
     # int32 key order == the 8-byte key order == canonical (t, y, x, p)
-    assert torch.equal(torch.argsort(k, stable=True), torch.argsort(pack_keys(t, x, y, p, 10**9), stable=True))
+    assert torch.equal(torch.argsort(k, stable=True),
+                       torch.argsort(pack_keys(t, x, y, p, 10**9, KEY64_LAYOUT), stable=True))

@@ -130,3 +130,22 @@ def test_large_batch_ops_vs_oracle():
     lb = ev.limit_bandwidth(cs, 3.3e7, 137)
     olb = oracle.limit_bandwidth(oracle.canonical_sort(ob), 3.3e7, 137)
     assert lb.same_events(olb) and lb.dropped_count == olb.dropped_count
+
+
+def test_canonical_sort_general_golden():
+    """canonical_sort of a batch outside the simulator's range (uint64 times
+    spanning > 2^31 us and >= 2^63, any int8 polarity) equals the reference's
+    lexsort (tests/golden/sort_general.npz, made by the reference itself)."""
+    g = dict(np.load(os.path.join(GOLD, "sort_general.npz")))
+    b = ev.EventBatch(g["t"].view(np.uint64), g["x"], g["y"], g["p"], dropped_count=9)
+    cs = ev.canonical_sort(b)
+    assert np.array_equal(cs.t.view(np.int64), g["cs_t"]) and np.array_equal(cs.x, g["cs_x"])
+    assert np.array_equal(cs.y, g["cs_y"]) and np.array_equal(cs.polarity, g["cs_p"])
+    assert cs.dropped_count == 9
+    # a batch only slightly outside (t-span 2^31) and a large random one vs the oracle
+    rng = np.random.default_rng(8)
+    for n, span in ((70_001, 1 << 31), (1_500_000, 1 << 45)):
+        b = ev.EventBatch(t=rng.integers(10, 10 + span, n).astype(np.uint64),
+                          x=rng.integers(0, 64, n).astype(np.uint16), y=rng.integers(0, 48, n).astype(np.uint16),
+                          polarity=rng.integers(-3, 3, n).astype(np.int8))
+        assert ev.canonical_sort(b).same_events(oracle.canonical_sort(oracle.OBatch(b.t, b.x, b.y, b.polarity)))

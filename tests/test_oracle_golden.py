@@ -118,3 +118,12 @@ def test_bench_fixture_first_frames_from_oracle(oracle_mod):
         assert fx["frames"][j] == {"count": len(b), "dropped": b.dropped_count,
                                    "reservations": b.reservation_count,
                                    "sha1": batch_sha1(b.t, b.x, b.y, b.polarity)}, j
+
+
+def test_oracle_canonical_sort_general(oracle_mod):
+    """The oracle's canonical_sort (uint64 t, int8 polarity) vs the reference's
+    lexsort on a batch outside the simulator's range (sort_general.npz)."""
+    g = load("sort_general.npz")
+    b = oracle_mod.canonical_sort(oracle_mod.OBatch(g["t"].view(np.uint64), g["x"], g["y"], g["p"]))
+    assert np.array_equal(b.t.view(np.int64), g["cs_t"]) and np.array_equal(b.x, g["cs_x"])
+    assert np.array_equal(b.y, g["cs_y"]) and np.array_equal(b.polarity, g["cs_p"])
