@@ -275,39 +275,53 @@ def verify_launch_shape(dev, T: int, frames: int = 150):
 
 
 def measure_t1(args, dev, cfg, phase0, rank, order=None):
-    """The same workload with one frame per launch (the reference's per-frame call
-    granularity), graph-replayed; reported next to the batched number.  order:
-    canonical (default) or pixel-major (generate_events_serial order, model.py:140)."""
+    """The same workload with one frame per evs_step (the reference's per-frame
+    call granularity), graph-replayed: (a) consecutive steps overlapped on two
+    streams (runtime.PipelinedSteps: step k+1's K1 runs while step k's
+    ordering finishes) -- the frame rate; (b) strictly one step after the other
+    -- the latency of one frame.  order: canonical (default) or pixel-major
+    (generate_events_serial order, model.py:140)."""
     import torch
 
     from paper_2602_15018_b200 import _lib
     from paper_2602_15018_b200 import events as ev
-    from paper_2602_15018_b200.runtime import StepEngine, StepShape
+    from paper_2602_15018_b200.runtime import PipelinedSteps, StepEngine, StepShape
     from paper_2602_15018_b200.synth import PERIOD_FRAMES, texture_frame
 
     P = W * H
     ring = device_texture_ring(W, H, PERIOD_FRAMES, DRIFT, phase0, dev)
-    st = ev.init_pixel_states(ev.IntensityFrame(W, H, 0, texture_frame(W, H, phase0)), cfg, seed=rank)
     order = _lib.EVS_ORDER_CANONICAL if order is None else order
-    eng = StepEngine(StepShape(1, 1, H, W, 8 * P, order, TICK, cfg.log_eps, REFR,
-                               st.uniform_thresholds), dev)
-    for k in range(5):
-        eng.launch(ring[k:k + 1], st.d_ref_log, st.d_last_event_t, t0=k * TICK, tick=TICK)
-    eng.capture([ring[(5 + i) % PERIOD_FRAMES:(5 + i) % PERIOD_FRAMES + 1] for i in range(PERIOD_FRAMES)],
-                st.d_ref_log, st.d_last_event_t, tick=TICK, t0=5 * TICK)
     reps = max(2, args.steps // PERIOD_FRAMES)
-    eng.replay()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        eng.replay()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    frames = reps * PERIOD_FRAMES
-    return {"frames_per_s": frames / (ms / 1e3), "us_per_frame": 1e3 * ms / frames, "frames": frames}
+    out = {}
+    for mode in ("pipelined", "serial"):
+        st = ev.init_pixel_states(ev.IntensityFrame(W, H, 0, texture_frame(W, H, phase0)), cfg, seed=rank)
+        shape = StepShape(1, 1, H, W, 8 * P, order, TICK, cfg.log_eps, REFR, st.uniform_thresholds)
+        runner = PipelinedSteps(shape, dev) if mode == "pipelined" else StepEngine(shape, dev)
+        eng0 = runner.engines[0] if mode == "pipelined" else runner
+        for k in range(5):
+            eng0.launch(ring[k:k + 1], st.d_ref_log, st.d_last_event_t, t0=k * TICK, tick=TICK)
+        if mode == "pipelined":
+            for k in range(5, 7):  # (kernel attributes of the second engine)
+                runner.engines[1].launch(ring[k:k + 1], st.d_ref_log, st.d_last_event_t, t0=k * TICK, tick=TICK)
+        k0 = 7 if mode == "pipelined" else 5
+        runner.capture([ring[(k0 + i) % PERIOD_FRAMES:(k0 + i) % PERIOD_FRAMES + 1] for i in range(PERIOD_FRAMES)],
+                       st.d_ref_log, st.d_last_event_t, tick=TICK, t0=k0 * TICK)
+        runner.replay()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            runner.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        frames = reps * PERIOD_FRAMES
+        out[mode] = {"frames_per_s": frames / (ms / 1e3), "us_per_frame": 1e3 * ms / frames, "frames": frames}
+    res = dict(out["pipelined"])
+    res["mode"] = "one frame per evs_step; consecutive steps overlapped on two streams (runtime.PipelinedSteps)"
+    res["one_step_after_the_other"] = out["serial"]
+    return res
 
 
 # --------------------------------------------------------------------------- the reference's own CPU path

@@ -71,6 +71,8 @@ typedef struct evs_step_params {
   int32_t validate;      /* 1: reject invalid frames before touching state */
   uint32_t epoch;        /* caller-maintained counter, see EVS_EPOCHS_PER_CALL */
   int32_t flags;         /* EVS_FLAG_* */
+  int32_t clock_stride;  /* device clock: steps of this workspace are clock_stride calls apart (0/1:
+                            consecutive; 2: two engines alternating, see evs_step_clock_init) */
 } evs_step_params;
 
 /* flags: t0 and epoch are taken from a clock kept in the workspace and
@@ -92,10 +94,10 @@ typedef struct evs_step_buffers {
   uint16_t* ev_y;          /* [S*T][capacity] */
   int8_t* ev_p;            /* [S*T][capacity] polarity +1/-1 */
   int64_t* counts;         /* [S*T] events written (= min(kept, capacity)) */
-  int64_t* dropped;        /* [S*T] EventBatch.dropped_count; -1: the tile-overflow area was
-                              exhausted, -2: a pixel would cross > 2^20 thresholds in one frame
-                              (+inf intensity without validation, or a corrupt ref_log)
-                              -- the call's outputs are then invalid */
+  int64_t* dropped;        /* [S*T] EventBatch.dropped_count (events beyond the capacity); -2: a
+                              pixel would cross > 2^20 thresholds in one frame (+inf intensity
+                              without validation, or a corrupt ref_log) -- the call's outputs
+                              are then invalid */
   int64_t* reservations;   /* [S*T] AggregationStats.reservation_count */
   int64_t* bad_pixel;      /* [1] must hold INT64_MAX on entry; receives the first
                               invalid flat index into frames (s*T*H*W + f*H*W + i) */

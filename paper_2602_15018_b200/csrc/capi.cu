@@ -175,7 +175,8 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   // read the frames once in the prologue (4 B/px per frame) instead
   const bool fuse_val = p->validate && p->frames >= 4;
   cudaError_t e = launch_prologue(b->frames, (int64_t)L.nseg * P, P, fuse_val ? 0 : p->validate, b->bad_pixel,
-                                  b->reservations, L.nseg, desc, (int64_t)p->frames * p->tick, zero2,
+                                  b->reservations, L.nseg, desc,
+                                  (int64_t)p->frames * p->tick * (p->clock_stride > 1 ? p->clock_stride : 1), zero2,
                                   L.n2, st);
   if (e != cudaSuccess) return EVS_ERR_CUDA;
   mark(1);

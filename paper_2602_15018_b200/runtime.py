@@ -145,7 +145,7 @@ class StepEngine:
                                           ctypes.c_void_p(_lib.stream_ptr()))
         _lib.check(rc, "evs_step_clock_init")
 
-    def _launch_dc(self, frames, ref_log, last_event_t, th_pos, th_neg, validate):
+    def _launch_dc(self, frames, ref_log, last_event_t, th_pos, th_neg, validate, stream=None, events=None):
         p, b = self.params, self.bufs
         p.validate = 1 if validate else 0
         b.frames = frames.data_ptr()
@@ -159,8 +159,13 @@ class StepEngine:
         b.ev_y, b.ev_p = self.ev_y.data_ptr(), self.ev_p.data_ptr()
         b.counts, b.dropped = self.info[0].data_ptr(), self.info[1].data_ptr()
         b.reservations, b.bad_pixel = self.info[2].data_ptr(), self.bad.data_ptr()
-        rc = self.lib.evs_step(ctypes.byref(p), ctypes.byref(b), ctypes.c_void_p(self.workspace.data_ptr()),
-                               ctypes.c_size_t(self.workspace.numel()), ctypes.c_void_p(_lib.stream_ptr()))
+        ws, nb = ctypes.c_void_p(self.workspace.data_ptr()), ctypes.c_size_t(self.workspace.numel())
+        sp = ctypes.c_void_p(_lib.stream_ptr(stream))
+        if events is None:
+            rc = self.lib.evs_step(ctypes.byref(p), ctypes.byref(b), ws, nb, sp)
+        else:
+            handles = (ctypes.c_void_p * len(events))(*[e.cuda_event if e is not None else None for e in events])
+            rc = self.lib.evs_step_profiled(ctypes.byref(p), ctypes.byref(b), ws, nb, sp, handles, len(events))
         _lib.check(rc, "evs_step")
 
     def replay(self) -> None:
@@ -190,6 +195,72 @@ class StepEngine:
 
     def reset_bad(self) -> None:
         self.bad.fill_(_lib.NO_BAD)
+
+
+class PipelinedSteps:
+    """Frame-by-frame stepping with consecutive steps overlapped: two
+    StepEngines of one shape (two workspaces and two output pools) alternate on
+    two streams, and step i+1 waits only for step i's K1 (the kernel that
+    writes the pixel state) -- its K1 then runs while step i's histogram,
+    scan and ordering kernels finish.  Used for one-frame steps (the
+    reference's per-frame call granularity), where every kernel is a single
+    partial wave.  Captured as one CUDA graph of an even number of steps with
+    each engine's clock advancing two steps per call (clock_stride = 2);
+    after a replay, step i's outputs are in engines[i % 2] until step i + 2.
+    """
+
+    def __init__(self, shape: StepShape, device):
+        self.engines = [StepEngine(shape, device), StepEngine(shape, device)]
+        self.shape = shape
+
+    def capture(self, windows, ref_log, last_event_t, th_pos=None, th_neg=None, tick: int = 1000, t0: int = 0,
+                validate: bool = True):
+        import torch
+
+        if len(windows) % 2:
+            raise ValueError("PipelinedSteps captures an even number of steps")
+        for e in self.engines:
+            e.params.flags = _lib.EVS_FLAG_DEVICE_CLOCK
+            e.params.tick = int(tick)
+            e.params.clock_stride = 2
+        self._tick, self._t0, self._n = int(tick), int(t0), len(windows)
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        k1_done = [torch.cuda.Event() for _ in windows]
+        for ev in k1_done:  # materialise the handles outside the capture
+            ev.record()
+        origin = torch.cuda.Stream()
+        origin.wait_stream(torch.cuda.current_stream())
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=origin):
+            for st in streams:
+                st.wait_stream(origin)
+            for i, win in enumerate(windows):
+                st = streams[i % 2]
+                if i > 0:
+                    st.wait_event(k1_done[i - 1])
+                self.engines[i % 2]._launch_dc(win, ref_log, last_event_t, th_pos, th_neg, validate, stream=st,
+                                               events=[None, None, k1_done[i], None, None])
+            for st in streams:
+                origin.wait_stream(st)
+        torch.cuda.current_stream().wait_stream(origin)
+        for e in self.engines:
+            e.params.flags = 0
+            e.params.clock_stride = 0
+        self._args = (windows, k1_done, streams)
+
+    def replay(self) -> None:
+        need = (self._n // 2) * _lib.EVS_EPOCHS_PER_CALL
+        for j, e in enumerate(self.engines):
+            if e.epochs.value + need > _lib.EVS_EPOCH_LIMIT:
+                e.workspace.zero_()
+                e.epochs.value = 1
+            e.params.flags = _lib.EVS_FLAG_DEVICE_CLOCK
+            e._clock_set(self._t0 + j * self.shape.frames * self._tick, e.epochs.value)
+            e.params.flags = 0
+        self.graph.replay()
+        for e in self.engines:
+            e.epochs.value += need
+        self._t0 += self._n * self.shape.frames * self._tick
 
 
 class PinnedPool:

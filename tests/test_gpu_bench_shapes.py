@@ -217,3 +217,44 @@ def test_acceptance_100_sequences_vs_oracle():
             assert b.same_events(oracle.canonical_sort(ob)), (seq_id, k)
         assert np.array_equal(s_ser.ref_log, ost.ref_log) and np.array_equal(s_par.ref_log, ost.ref_log)
         assert np.array_equal(s_par.last_event_t, ost.last_event_t)
+
+
+@pytest.mark.parametrize("W,H,order,refr", [(1280, 720, 1, 100), (640, 480, 0, 0)])
+def test_pipelined_one_frame_steps_match_oracle(W, H, order, refr):
+    """runtime.PipelinedSteps (bench.py's per-frame rate): one-frame steps on two
+    engines / streams, step i+1 waiting only for step i's K1, replayed as one
+    graph; every frame's events (canonical or pixel-major) and the state vs
+    the oracle."""
+    import torch
+
+    from paper_2602_15018_b200.runtime import PipelinedSteps, StepShape
+
+    import bench
+
+    P, TICK = W * H, 1000
+    dev = torch.device("cuda")
+    ring = bench.device_texture_ring(W, H, 50, 0.02, 0.0, dev)
+    host = ring.cpu().numpy()
+    cfg = ev.EventCameraConfig(c_pos=0.15, c_neg=0.15, refractory_us=refr)
+    st = ev.init_pixel_states(ev.IntensityFrame(W, H, 0, texture_frame(W, H, 0.0)), cfg, seed=0)
+    ost = oracle.init_state(host[0], c_pos=0.15, c_neg=0.15, refractory_us=refr, seed=0)
+    pipe = PipelinedSteps(StepShape(1, 1, H, W, 8 * P, order, TICK, cfg.log_eps, refr, st.uniform_thresholds), dev)
+    k = 0
+    for e in pipe.engines:  # an eager step on each engine first (as bench.py does)
+        e.launch(ring[k:k + 1], st.d_ref_log, st.d_last_event_t, t0=k * TICK, tick=TICK)
+        ob = oracle.generate(ost, host[k], k * TICK, (k + 1) * TICK, refractory_us=refr)
+        k += 1
+    pipe.capture([ring[k:k + 1], ring[k + 1:k + 2]], st.d_ref_log, st.d_last_event_t, tick=TICK, t0=k * TICK)
+    for rep in range(3):
+        pipe.replay()
+        torch.cuda.synchronize()
+        for j, e in enumerate(pipe.engines):  # the graph's frames are always ring[2] and ring[3]
+            counts, dropped, res, bad = e.fetch_info()
+            assert bad == _lib.NO_BAD
+            ob = oracle.generate(ost, host[2 + j], k * TICK, (k + 1) * TICK, refractory_us=refr)
+            if order == 1:
+                ob = oracle.canonical_sort(ob)
+            _same_segment(e, 0, counts, dropped, res, ob, (rep, j))
+            k += 1
+        assert np.array_equal(st.d_ref_log.cpu().numpy(), ost.ref_log)
+        assert np.array_equal(st.d_last_event_t.cpu().numpy(), ost.last_event_t)
