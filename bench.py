@@ -215,13 +215,14 @@ def _sha1(arrays) -> str:
     return h.hexdigest()
 
 
-def verify_launch_shape(dev, T: int, frames: int = 150):
+def verify_launch_shape(dev, T: int, frames: int = 150, pipelined: bool = False):
     """Self-check of the benchmarked launch shape (HD, T frames per evs_step,
     capacity 8P, fused validation, CUDA-graph replay with the device clock)
     against the oracle fixture tests/golden/bench_hd_t50.json (per-frame
     counts, drops, reservations, SHA-1 of the canonical events; the state).
     The first step runs eagerly, the following ones as graph replays, exactly
-    like the timed region.  Returns the list of mismatching frames."""
+    like the timed region (pipelined: the replays alternate two engines on two
+    streams, runtime.PipelinedSteps).  Returns the list of mismatching frames."""
     import torch
 
     from paper_2602_15018_b200 import _lib
@@ -241,28 +242,49 @@ def verify_launch_shape(dev, T: int, frames: int = 150):
                                st.uniform_thresholds), dev)
     nsteps = (frames + T - 1) // T
     bad = []
-    for i in range(nsteps):
-        win = ring[(i * T) % ring_len:(i * T) % ring_len + T]
-        if i == 0:
-            eng.launch(win, st.d_ref_log, st.d_last_event_t, t0=0, tick=TICK, validate=True)
-        else:
-            if i == 1 or (T % PERIOD_FRAMES):  # (windows repeat when T is a multiple of the period)
-                eng.capture([win], st.d_ref_log, st.d_last_event_t, tick=TICK, t0=i * T * TICK)
-            eng.replay()
-        torch.cuda.synchronize()
-        counts, dropped, res, badpx = eng.fetch_info()
+
+    def check(e, i):
+        counts, dropped, res, badpx = e.fetch_info()
         if badpx != _lib.NO_BAD:
-            return ["invalid frame"]
+            bad.append(f"invalid frame in step {i}")
+            return
         for f in range(T):
             j = i * T + f
             if j >= frames:
                 break
             n = int(counts[f])
             got = {"count": n, "dropped": int(dropped[f]), "reservations": int(res[f]),
-                   "sha1": _sha1([eng.ev_t[f, :n].cpu().numpy(), eng.ev_x[f, :n].cpu().numpy(),
-                                  eng.ev_y[f, :n].cpu().numpy(), eng.ev_p[f, :n].cpu().numpy()])}
+                   "sha1": _sha1([e.ev_t[f, :n].cpu().numpy(), e.ev_x[f, :n].cpu().numpy(),
+                                  e.ev_y[f, :n].cpu().numpy(), e.ev_p[f, :n].cpu().numpy()])}
             if got != fx["frames"][j]:
                 bad.append(j)
+
+    win0 = ring[0:T]
+    eng.launch(win0, st.d_ref_log, st.d_last_event_t, t0=0, tick=TICK, validate=True)
+    torch.cuda.synchronize()
+    check(eng, 0)
+    if pipelined and nsteps >= 3:
+        from paper_2602_15018_b200.runtime import PipelinedSteps
+
+        pipe = PipelinedSteps(eng.shape, dev)
+        pipe.engines[0] = eng
+        i = 1
+        while i < nsteps:
+            wins = [ring[((i + j) * T) % ring_len:((i + j) * T) % ring_len + T] for j in range(2)]
+            pipe.capture(wins, st.d_ref_log, st.d_last_event_t, tick=TICK, t0=i * T * TICK)
+            pipe.replay()
+            torch.cuda.synchronize()
+            for j in range(2):
+                if i + j < nsteps:
+                    check(pipe.engines[j], i + j)
+            i += 2
+    for i in range(1, nsteps if not (pipelined and nsteps >= 3) else 1):
+        win = ring[(i * T) % ring_len:(i * T) % ring_len + T]
+        if i == 1 or (T % PERIOD_FRAMES):  # (windows repeat when T is a multiple of the period)
+            eng.capture([win], st.d_ref_log, st.d_last_event_t, tick=TICK, t0=i * T * TICK)
+        eng.replay()
+        torch.cuda.synchronize()
+        check(eng, i)
     if nsteps * T == frames == len(fx["frames"]):
         import hashlib
 
@@ -571,12 +593,23 @@ def run_ours(args):
                 gathered["n"] = n
 
     # timed region
+    runner = eng
     if extra is None:
         # CUDA graph of G steps (one per window); the step clock advances on the device
         G = max(g for g in range(1, min(K, 64) + 1) if K % g == 0 and (g % len(windows) == 0 or g < len(windows)))
         k_next = state["k"]
-        eng.capture([windows[(k_next + i) % len(windows)] for i in range(G)], ref, last, tick=TICK,
-                    t0=k_next * T * TICK)
+        if args.pipelined and G % 2 == 0:
+            from paper_2602_15018_b200.runtime import PipelinedSteps
+
+            runner = PipelinedSteps(eng.shape, dev)
+            runner.engines[0] = eng
+            for _ in range(2):  # (kernel attributes of the second engine) -- untimed
+                runner.engines[1].launch(windows[state["k"] % len(windows)], ref, last, t0=state["k"] * T * TICK,
+                                         tick=TICK, validate=True, stream=stream)
+                state["k"] += 1
+            k_next = state["k"]
+        runner.capture([windows[(k_next + i) % len(windows)] for i in range(G)], ref, last, tick=TICK,
+                       t0=k_next * T * TICK)
         reps = K // G
         launches = K * 5 + reps
     else:
@@ -594,7 +627,7 @@ def run_ours(args):
     e0.record(stream)
     if extra is None:
         for _ in range(reps):
-            eng.replay()
+            runner.replay()
         state["k"] += K
     else:
         for i in range(K):
@@ -697,10 +730,12 @@ def run_ours(args):
                      "h2d_bytes_per_step": 4 * P, "d2h_bytes_per_step": int(d2h / ke),
                      "api": "paper_2602_15018_b200.events.generate_events_parallel (drop-in, one frame per call)"}
         # self-check of the timed launch shape against the oracle fixture (untimed)
-        mism = verify_launch_shape(dev, T)
+        mism = verify_launch_shape(dev, T, pipelined=bool(args.pipelined))
         self_check = {"fixture": "tests/golden/bench_hd_t50.json (oracle, 150 HD frames: per-frame counts, drops, "
                                  "reservations, SHA-1 of the canonical events; final state)",
-                      "launch": f"same StepShape (T={T}), eager step then CUDA-graph replays", "frames": 150,
+                      "launch": f"same StepShape (T={T}), eager step then CUDA-graph replays"
+                                + (" of two engines on two streams (PipelinedSteps)" if args.pipelined else ""),
+                      "frames": 150,
                       "mismatches": [str(m) for m in mism[:10]], "ok": not mism}
         if T != 1 and args.compare_t1:
             per_frame = measure_t1(args, dev, ecfg, phases[0], rank)
@@ -764,6 +799,8 @@ def main():
     ap.add_argument("--frames-per-step", type=int, default=0, help="0: the config's default (HD: 50)")
     ap.add_argument("--config", default="2", choices=sorted(CONFIGS))
     ap.add_argument("--compare-t1", type=int, default=1)
+    ap.add_argument("--pipelined", type=int, default=1,
+                    help="1: consecutive steps on two engines / streams (runtime.PipelinedSteps)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()

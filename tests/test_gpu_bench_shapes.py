@@ -90,6 +90,7 @@ def test_bench_self_check_fixture():
     import bench
 
     assert bench.verify_launch_shape(torch.device("cuda"), 50) == []
+    assert bench.verify_launch_shape(torch.device("cuda"), 50, pipelined=True) == []
 
 
 def _sim_run(W, H, S, T, c, refr, steps, cap=None, noise_hz=0.0, canonical=True):
