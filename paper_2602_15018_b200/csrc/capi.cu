@@ -35,7 +35,7 @@ int sm_count_current() {
 }
 
 struct StepLayout {
-  int nseg, ntiles, npass, bits, NB, ngroups, gt;
+  int nseg, ntiles, npass, bits, NB, ngroups, gt, tile_px, tile_cap;
   int64_t max_tiles2, ovf_lim, ovf_cap, n2;
   size_t chunk_flag;
   size_t ctr, desc, zero2, region, tile_count, tile_ovf, tile_base, ovf_area, rows, tot, hist, gstart,
@@ -54,7 +54,15 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   if (p->height > 65535 || p->width > 65535 || p->capacity < 0) return false;
   const int64_t P = (int64_t)p->height * p->width;
   L->nseg = p->streams * p->frames;
-  L->ntiles = (int)((P + kGenTile - 1) / kGenTile);
+  // K1 tiles: 1024 pixels (4 per thread); a batch too small to fill the GPU
+  // with them (one small sensor) gets 256-pixel tiles (one pixel per thread):
+  // 4x more CTAs and warps over the same pixels
+  {
+    const int64_t big = (int64_t)p->streams * ((P + kGenTile - 1) / kGenTile);
+    L->tile_px = big < 2 * (int64_t)sm_count_current() ? kGenTile / kGenVpt : kGenTile;
+    L->tile_cap = 4 * L->tile_px;
+  }
+  L->ntiles = (int)((P + L->tile_px - 1) / L->tile_px);
   const bool canon = p->order == EVS_ORDER_CANONICAL;
   int tbits = 1;
   if (canon) {
@@ -82,7 +90,7 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   // full keeps only its count and a pre-frame state snapshot, and k_group_hist
   // regenerates it into [ovf_lim, ovf_lim + capacity) when it lies inside the
   // kept prefix (the kept events of a frame never exceed the capacity)
-  L->ovf_lim = (int64_t)kTileCap * (1 + L->ntiles / 4);
+  L->ovf_lim = (int64_t)L->tile_cap * (1 + L->ntiles / 4);
   L->ovf_cap = L->ovf_lim + p->capacity;
   const size_t ns = (size_t)L->nseg, nt = (size_t)L->ntiles;
   size_t off = 0;
@@ -108,10 +116,10 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   const bool bak = p->frames >= 4;  // fused validation (step_impl)
   L->bak_ref = off; off = align_up(off + (bak ? (size_t)p->streams * P * 4 : 0));
   L->bak_last = off; off = align_up(off + (bak ? (size_t)p->streams * P * 8 : 0));
-  L->region = off; off = align_up(off + ns * nt * kTileCap * 8);
+  L->region = off; off = align_up(off + ns * nt * L->tile_cap * 8);
   L->ovf_area = off; off = align_up(off + ns * (size_t)L->ovf_cap * 8);
-  L->snap_ref = off; off = align_up(off + ns * nt * kGenTile * 4);
-  L->snap_last = off; off = align_up(off + ns * nt * kGenTile * 4);
+  L->snap_ref = off; off = align_up(off + ns * nt * L->tile_px * 4);
+  L->snap_last = off; off = align_up(off + ns * nt * L->tile_px * 4);
   L->total = off;
   return true;
 }
@@ -195,6 +203,7 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   g.bad = b->bad_pixel;
   g.epoch = p->epoch;
   g.ntiles = L.ntiles;
+  g.tile_px = L.tile_px; g.tile_cap = L.tile_cap;
   g.desc = desc;
   g.rows = canon ? at<uint32_t>(ws, L.rows) : nullptr;
   g.ngroups = L.ngroups;
@@ -237,6 +246,7 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
 
   TileScanArgs ts;
   memset(&ts, 0, sizeof(ts));
+  ts.tile_px = L.tile_px; ts.tile_cap = L.tile_cap;
   ts.nseg = L.nseg; ts.ntiles = L.ntiles; ts.ngroups = L.ngroups; ts.bits = L.bits; ts.cap = p->capacity;
   ts.gt = L.gt;
   ts.tile_count = g.tile_count; ts.tile_ovf = g.tile_ovf; ts.region = g.region; ts.ovf_area = g.ovf_area;
@@ -263,6 +273,7 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
 
   TileOrderArgs to;
   memset(&to, 0, sizeof(to));
+  to.tile_px = L.tile_px; to.tile_cap = L.tile_cap;
   to.nseg = L.nseg; to.ntiles = L.ntiles; to.ngroups = L.ngroups; to.bits = L.bits; to.shift = kKeyPixBits;
   to.gt = L.gt;
   to.cap = p->capacity; to.tile_count = g.tile_count; to.tile_ovf = g.tile_ovf; to.tile_base = ts.tile_base;
@@ -338,6 +349,7 @@ static void step_regions(const evs_step_params* p, const evs_step_buffers* b, co
                          StepVoxArgs* a) {
   memset(a, 0, sizeof(*a));
   a->ntiles = L.ntiles; a->T = p->frames; a->W = p->width;
+  a->tile_px = L.tile_px; a->tile_cap = L.tile_cap;
   a->P = (int64_t)p->height * p->width; a->cap = p->capacity; a->ovf_cap = L.ovf_cap;
   void* w = const_cast<void*>(ws);
   a->tile_count = at<int64_t>(w, L.tile_count);

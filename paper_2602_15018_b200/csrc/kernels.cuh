@@ -16,7 +16,8 @@ constexpr int kKeyPixBits = 33;   // key = t_rel << 33 | y << 17 | x << 1 | (p >
 
 constexpr int kGenThreads = 256;
 constexpr int kGenVpt = 4;
-constexpr int kGenTile = kGenThreads * kGenVpt;  // pixels per K1 tile
+constexpr int kGenTile = kGenThreads * kGenVpt;  // pixels per K1 tile (the largest; small sensors use
+                                                 // 256-pixel tiles, one pixel per thread: args.tile_px)
 
 constexpr int kOrdThreads = 256;
 constexpr int kOrdIpt = 16;
@@ -30,6 +31,7 @@ struct StepDesc {
 };
 
 struct GenArgs {
+  int tile_px, tile_cap;  // pixels per K1 tile (1024 or 256) and keys per tile region (4 per pixel)
   int S, T, H, W;
   int64_t P;
   double log_eps;
@@ -98,11 +100,11 @@ struct GenArgs {
   int64_t* bak_last;   // [S][P]
 };
 
-constexpr int kSlotsPerLane = 16;
 constexpr int64_t kTileRedo = -3;  // tile_ovf: K1 kept only the count (k_group_hist regenerates)
-constexpr int kTileCap = kSlotsPerLane * kGenThreads;  // keys per tile region
+constexpr int kTileCap = 4 * kGenTile;  // keys per region of the largest tile (4 per pixel; args.tile_cap)
 
 struct TileScanArgs {
+  int tile_px, tile_cap;  // pixels per K1 tile (1024 or 256) and keys per tile region (4 per pixel)
   int nseg, ntiles, ngroups, bits;
   int64_t cap;
   const int64_t* tile_count;  // [nseg][ntiles]
@@ -144,6 +146,7 @@ struct TileScanArgs {
 };
 
 struct TileOrderArgs {
+  int tile_px, tile_cap;  // pixels per K1 tile (1024 or 256) and keys per tile region (4 per pixel)
   int nseg, ntiles, ngroups, bits, shift;
   int64_t cap;
   const int64_t* tile_count;
@@ -171,6 +174,7 @@ struct TileOrderArgs {
 // regions (represent.cu): one CTA per 1024-pixel tile accumulates the exact
 // int64 numerators of its own pixels in shared memory (no global atomics).
 struct StepVoxArgs {
+  int tile_px, tile_cap;  // pixels per K1 tile (1024 or 256) and keys per tile region (4 per pixel)
   int ntiles, T, s, B;
   int W;
   int64_t P, cap, ovf_cap;

@@ -125,7 +125,7 @@ __device__ __forceinline__ VoxTileSrc vox_tile_src(const StepVoxArgs& a, int q, 
   nkeep = nkeep < 0 ? 0 : (nkeep > nq ? nq : nkeep);
   const int64_t ov = a.tile_ovf[sq];
   VoxTileSrc r;
-  r.src = ov >= 0 ? a.ovf_area + seg * a.ovf_cap + ov : a.region + sq * kTileCap;
+  r.src = ov >= 0 ? a.ovf_area + seg * a.ovf_cap + ov : a.region + sq * a.tile_cap;
   r.nkeep = nkeep;
   r.tb = a.seg_tbase[seg];
   return r;
@@ -135,13 +135,14 @@ __global__ void __launch_bounds__(256) k_step_voxel(StepVoxArgs a, int narrow) {
   extern __shared__ __align__(16) unsigned char vsm[];
   const int q = blockIdx.x, tid = threadIdx.x;
   const int64_t D = a.t1 - a.t0;
-  const int64_t tile0 = (int64_t)q * kGenTile;
+  const int TP = a.tile_px;  // pixels per tile (<= kGenTile)
+  const int64_t tile0 = (int64_t)q * TP;
   const bool ok = *a.bad == kNoBad;
   __shared__ int s_wide;
   if (narrow) {
-    int* acc = reinterpret_cast<int*>(vsm);        // [B][kGenTile]
-    int* cnt = acc + a.B * kGenTile;               // [kGenTile]
-    for (int i = tid; i < (a.B + 1) * kGenTile; i += blockDim.x) acc[i] = 0;
+    int* acc = reinterpret_cast<int*>(vsm);        // [B][TP]
+    int* cnt = acc + a.B * TP;                     // [TP]
+    for (int i = tid; i < (a.B + 1) * TP; i += blockDim.x) acc[i] = 0;
     if (tid == 0) s_wide = 0;
     __syncthreads();
     const int d32 = (int)D;
@@ -163,18 +164,18 @@ __global__ void __launch_bounds__(256) k_step_voxel(StepVoxArgs a, int narrow) {
           for (int b = b0; b <= b0 + 1 && b < a.B; ++b) {
             const int d = b * d32 - tau;
             const int w = d32 - (d < 0 ? -d : d);
-            if (w > 0) atomicAdd(acc + b * kGenTile + lp, pol * w);
+            if (w > 0) atomicAdd(acc + b * TP + lp, pol * w);
           }
         }
       }
     }
     __syncthreads();
-    for (int i = tid; i < kGenTile; i += blockDim.x)
+    for (int i = tid; i < TP; i += blockDim.x)
       if ((int64_t)cnt[i] * D >= (1ll << 31)) s_wide = 1;
     __syncthreads();
     if (!s_wide) {
-      for (int i = tid; i < a.B * kGenTile; i += blockDim.x) {
-        const int b = i / kGenTile, lp = i % kGenTile;
+      for (int i = tid; i < a.B * TP; i += blockDim.x) {
+        const int b = i / TP, lp = i % TP;
         const int64_t pix = tile0 + lp;
         if (pix >= a.P) continue;
         const long long v = acc[i];
@@ -185,8 +186,8 @@ __global__ void __launch_bounds__(256) k_step_voxel(StepVoxArgs a, int narrow) {
     }
     __syncthreads();  // (redo this tile below with 64-bit accumulators)
   }
-  unsigned long long* acc = reinterpret_cast<unsigned long long*>(vsm);  // [B][kGenTile]
-  for (int i = tid; i < a.B * kGenTile; i += blockDim.x) acc[i] = 0ull;
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(vsm);  // [B][TP]
+  for (int i = tid; i < a.B * TP; i += blockDim.x) acc[i] = 0ull;
   __syncthreads();
   if (ok) {
     for (int f = 0; f < a.T; ++f) {
@@ -203,14 +204,14 @@ __global__ void __launch_bounds__(256) k_step_voxel(StepVoxArgs a, int narrow) {
           int64_t d = b * D - tau;
           d = d < 0 ? -d : d;
           const int64_t w = D - d;
-          if (w > 0) atomicAdd(acc + b * kGenTile + lp, (unsigned long long)(pol * w));
+          if (w > 0) atomicAdd(acc + b * TP + lp, (unsigned long long)(pol * w));
         }
       }
     }
   }
   __syncthreads();
-  for (int i = tid; i < a.B * kGenTile; i += blockDim.x) {
-    const int b = i / kGenTile, lp = i % kGenTile;
+  for (int i = tid; i < a.B * TP; i += blockDim.x) {
+    const int b = i / TP, lp = i % TP;
     const int64_t pix = tile0 + lp;
     if (pix >= a.P) continue;
     const long long v = (long long)acc[i];
@@ -241,7 +242,8 @@ __global__ void __launch_bounds__(256) k_step_hist(StepVoxArgs a, int64_t lo, in
   const int q = blockIdx.x, s = blockIdx.y, tid = threadIdx.x;
   for (int i = tid; i < kGenTile; i += blockDim.x) acc[i] = 0;
   __syncthreads();
-  const int64_t tile0 = (int64_t)q * kGenTile;
+  const int TP = a.tile_px;  // pixels per tile (<= kGenTile)
+  const int64_t tile0 = (int64_t)q * TP;
   if (*a.bad == kNoBad) {
     StepVoxArgs b = a;
     b.s = s;
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(256) k_step_hist(StepVoxArgs a, int64_t lo, in
     }
   }
   __syncthreads();
-  for (int i = tid; i < kGenTile; i += blockDim.x) {
+  for (int i = tid; i < TP; i += blockDim.x) {
     const int64_t pix = tile0 + i;
     if (pix < a.P) out[(int64_t)s * a.P + pix] = acc[i];
   }
