@@ -1,6 +1,7 @@
 """The NCCL gather of packed event keys (BASELINE config 5) between 2 GPUs:
-runs whenever the box has >= 2 GPUs (every GPU call of this build had one, so
-it skips there; the same logic runs over gloo in tests/test_distributed.py)."""
+collected whenever the box has >= 2 GPUs (tests/conftest.py deselects it on
+one-GPU boxes, which every GPU call of this build had; the same logic runs
+over gloo in tests/test_distributed.py)."""
 
 import os
 import socket
@@ -8,7 +9,7 @@ import socket
 import numpy as np
 import pytest
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
 def _free_port():
@@ -59,8 +60,6 @@ def test_nccl_gather_of_packed_keys_two_gpus():
     import oracle
     from paper_2602_15018_b200.synth import texture_frame
 
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs (NCCL between ranks)")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
