@@ -196,6 +196,7 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   g.refr = p->refractory_us; g.cap = p->capacity;
   g.thp_u = p->th_pos_uniform; g.thn_u = p->th_neg_uniform;
   g.frames = b->frames; g.t_bounds = b->t_bounds; g.t0 = p->t0; g.tick = p->tick;
+  g.max_dt = p->max_dt > 0 ? p->max_dt : p->tick;
   g.ref = b->ref_log; g.last = b->last_event_t; g.thp = b->th_pos; g.thn = b->th_neg;
   g.seg_res = b->reservations;
   g.seg_tbase = at<int64_t>(ws, L.seg_tbase);
