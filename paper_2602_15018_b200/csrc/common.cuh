@@ -95,11 +95,21 @@ __device__ __forceinline__ T block_excl_scan_1s(T v, T* buf, T* total) {
   if (lane == 31) buf[warp] = inc;
   __syncthreads();
   T pre = T(0), tot = T(0);
+  if constexpr (NW == 8 && sizeof(T) == 4) {  // the 8 warp totals in two 16-byte loads (buf 16-byte aligned)
+    const uint4 q0 = reinterpret_cast<const uint4*>(buf)[0], q1 = reinterpret_cast<const uint4*>(buf)[1];
+    const T x[8] = {(T)q0.x, (T)q0.y, (T)q0.z, (T)q0.w, (T)q1.x, (T)q1.y, (T)q1.z, (T)q1.w};
 #pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    const T x = buf[w];
-    pre += w < warp ? x : T(0);
-    tot += x;
+    for (int w = 0; w < NW; ++w) {
+      pre += w < warp ? x[w] : T(0);
+      tot += x[w];
+    }
+  } else {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const T x = buf[w];
+      pre += w < warp ? x : T(0);
+      tot += x;
+    }
   }
   *total = tot;
   return pre + inc - v;
