@@ -72,6 +72,7 @@ struct GenArgs {
   double rth_pos, rth_neg;  // 1/th for uniform thresholds (set by launch_generate)
   float rthp_f, rthn_f;     // the same rounded to f32 (certified lite math)
   double w_inv;             // 1 / W (set by launch_generate)
+  float thp_pf, thn_pf;     // th * (1 - 1e-4) of the uniform thresholds (prefilter)
   int64_t max_dt;           // bound of t_now - t_prev over the call (params.max_dt, else tick)
   // per-tile event regions (no inter-tile dependency in K1):
   uint64_t* region;          // [nseg][ntiles][kTileCap] pixel-major keys
