@@ -40,6 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     objs = []
     extra = ["-Xptxas", "-v"] if verbose else []
+    extra += os.environ.get("EVS_NVCC_EXTRA", "").split()  # experiment flags (-D...)
     for src in _sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [NVCC, *FLAGS, *extra, "-c", src, "-o", obj]
