@@ -23,6 +23,10 @@ constexpr int kOrdThreads = 256;
 constexpr int kOrdIpt = 16;
 constexpr int kOrdTile = kOrdThreads * kOrdIpt;  // keys per K2 tile
 
+// Raise a kernel's dynamic shared-memory limit to the opt-in maximum, once per
+// (device, kernel); thread-safe (k1_list.cu).
+void smem_optin(const void* func);
+
 // Device-resident step clock (EVS_FLAG_DEVICE_CLOCK): lets a captured CUDA
 // graph replay steps whose start time and lookback epoch advance on device.
 struct StepDesc {

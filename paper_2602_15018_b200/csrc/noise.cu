@@ -447,12 +447,8 @@ static cudaError_t launch_noise(const NoiseBatch& b, const NoiseLayout* Ls, int 
   }
   k_noise_walk<false><<<dim3((unsigned)gw, nf), 256, 0, st>>>(b);
   {
-    static bool raised = false;
     const int smem = 2 * kNsChunk * (int)sizeof(int64_t);
-    if (!raised) {
-      cudaFuncSetAttribute(k_noise_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      raised = true;
-    }
+    smem_optin(reinterpret_cast<const void*>(k_noise_scan));
     k_noise_scan<<<dim3(1, nf), 1024, smem, st>>>(b);
   }
   k_noise_walk<true><<<dim3((unsigned)gw, nf), 256, 0, st>>>(b);

@@ -85,17 +85,11 @@ cudaError_t launch_prologue(const float* frames, int64_t nframes_px, int64_t P, 
   return cudaGetLastError();
 }
 
-// Raise a kernel's dynamic-smem limit once per process (not per launch).
+// Raise a kernel's dynamic-smem limit once per (device, kernel) (smem_optin).
 template <typename K>
 static void ensure_smem(K k, size_t smem) {
-  static const void* done[64];
-  static int ndone = 0;
   if (smem <= 48 * 1024) return;
-  const void* key = reinterpret_cast<const void*>(k);
-  for (int i = 0; i < ndone; ++i)
-    if (done[i] == key) return;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  if (ndone < 64) done[ndone++] = key;
+  smem_optin(reinterpret_cast<const void*>(k));
 }
 
 

@@ -222,12 +222,7 @@ __global__ void __launch_bounds__(256) k_step_voxel(StepVoxArgs a, int narrow) {
 
 cudaError_t launch_step_voxel(const StepVoxArgs& a, cudaStream_t st) {
   const size_t smem = (size_t)a.B * kGenTile * sizeof(long long);  // >= the narrow (B + 1) x 4 B
-  static bool raised = false;
-  if (!raised) {
-    cudaFuncSetAttribute(k_step_voxel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((size_t)kStepVoxMaxBins * kGenTile * sizeof(long long)));
-    raised = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_step_voxel));
   const int narrow = (int64_t)(a.B - 1) * (a.t1 - a.t0) < (1ll << 30) ? 1 : 0;
   k_step_voxel<<<a.ntiles, 256, smem, st>>>(a, narrow);
   return cudaGetLastError();
