@@ -617,6 +617,8 @@ def run_ours(args):
         launches = None
         for w in range(2):  # warm the extras
             extra(state["k"] if ck == "5" else w)
+        if ck == "4":
+            sim.result()  # (untimed) a fetched step: the next steps' tile groups follow its density
     sampler = ClockSampler(local)
     if world > 1:
         dist.barrier()

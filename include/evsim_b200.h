@@ -73,6 +73,10 @@ typedef struct evs_step_params {
   int32_t flags;         /* EVS_FLAG_* */
   int32_t clock_stride;  /* device clock: steps of this workspace are clock_stride calls apart (0/1:
                             consecutive; 2: two engines alternating, see evs_step_clock_init) */
+  int64_t keys_hint;     /* expected events per (stream, frame), e.g. the previous call's mean
+                            (0: none).  Performance only: it sizes the tile groups of the
+                            ordering pass (the workspace does not depend on it); results are
+                            identical for any value */
 } evs_step_params;
 
 /* flags: t0 and epoch are taken from a clock kept in the workspace and

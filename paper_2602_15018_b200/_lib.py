@@ -47,6 +47,7 @@ class StepParams(ctypes.Structure):
         ("t0", ctypes.c_int64), ("tick", ctypes.c_int64), ("max_dt", ctypes.c_int64),
         ("order", ctypes.c_int32), ("validate", ctypes.c_int32),
         ("epoch", ctypes.c_uint32), ("flags", ctypes.c_int32), ("clock_stride", ctypes.c_int32),
+        ("keys_hint", ctypes.c_int64),
     ]
 
 

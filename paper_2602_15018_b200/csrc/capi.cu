@@ -35,7 +35,7 @@ int sm_count_current() {
 }
 
 struct StepLayout {
-  int nseg, ntiles, npass, bits, NB, ngroups, gt, tile_px, tile_cap;
+  int nseg, ntiles, npass, bits, NB, ngroups, gt, rows_stride, tile_px, tile_cap;
   int64_t max_tiles2, ovf_lim, ovf_cap, n2;
   size_t chunk_flag;
   size_t ctr, desc, zero2, region, tile_count, tile_ovf, tile_base, ovf_area, rows, tot, hist, gstart,
@@ -84,6 +84,22 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
     for (int g = kMaxGroupTiles; g > 1; --g)
       if ((int64_t)((L->ntiles + g - 1) / g) * L->nseg >= want) { L->gt = g; break; }
   }
+  // a call of many K2 CTAs (>= 8 waves at the largest groups) may use groups
+  // down to half that size when the caller expects dense frames (keys_hint:
+  // one K2 chunk of keys per group -- each chunk pays K2's per-bin column
+  // prefix, scan and barriers, and one-chunk CTAs turn over fastest; HD T=50:
+  // K2 0.429 -> 0.399 ms with 8-tile groups, while a sparse DAVIS stream is
+  // slower with them).  The rows are always stored for the smallest choice,
+  // so the workspace does not depend on the hint.
+  int gt_min = L->gt;
+  if ((int64_t)((L->ntiles + L->gt - 1) / L->gt) * L->nseg >= 16 * (int64_t)sm_count_current())
+    gt_min = L->gt / 2 > 1 ? L->gt / 2 : 1;
+  L->rows_stride = (L->ntiles + gt_min - 1) / gt_min;
+  if (p->keys_hint > 0 && gt_min < L->gt) {
+    const int64_t per_chunk = tile_order_chunk_keys(L->tile_px, canon ? 0 : 1, L->bits);
+    const int64_t g = per_chunk * L->ntiles / p->keys_hint;  // tiles whose mean keys fill one chunk
+    L->gt = (int)(g < gt_min ? gt_min : (g > L->gt ? L->gt : g));
+  }
   L->ngroups = (L->ntiles + L->gt - 1) / L->gt;
   // spill area per segment: [0, ovf_lim) is claimed by K1 tiles whose keys do
   // not fit their region (atomic cursor, arrival order); a tile that finds it
@@ -105,7 +121,7 @@ bool step_layout(const evs_step_params* p, StepLayout* L) {
   L->tile_base = off; off = align_up(off + ns * nt * 8);
   L->seg_tbase = off; off = align_up(off + ns * 8);
   L->seg_dt = off; off = align_up(off + ns * 8);
-  L->rows = off; off = align_up(off + (canon ? ns * L->ngroups * L->NB * 4 : 0));
+  L->rows = off; off = align_up(off + (canon ? ns * L->rows_stride * L->NB * 4 : 0));
   L->tot = off; off = align_up(off + ns * L->NB * 4);
   L->hist = off; off = align_up(off + (L->npass > 1 ? ns * L->npass * kHistReps * L->NB * 4 : 0));
   L->gstart = off; off = align_up(off + ns * L->NB * 4);
@@ -250,6 +266,7 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   ts.tile_px = L.tile_px; ts.tile_cap = L.tile_cap;
   ts.nseg = L.nseg; ts.ntiles = L.ntiles; ts.ngroups = L.ngroups; ts.bits = L.bits; ts.cap = p->capacity;
   ts.gt = L.gt;
+  ts.rows_stride = L.rows_stride;
   ts.tile_count = g.tile_count; ts.tile_ovf = g.tile_ovf; ts.region = g.region; ts.ovf_area = g.ovf_area;
   ts.ovf_cap = L.ovf_cap; ts.tile_base = at<int64_t>(ws, L.tile_base);
   // regeneration of the tiles K1 could not store (k_group_hist)
@@ -277,6 +294,7 @@ static evs_status step_impl(const evs_step_params* p, const evs_step_buffers* b,
   to.tile_px = L.tile_px; to.tile_cap = L.tile_cap;
   to.nseg = L.nseg; to.ntiles = L.ntiles; to.ngroups = L.ngroups; to.bits = L.bits; to.shift = kKeyPixBits;
   to.gt = L.gt;
+  to.rows_stride = L.rows_stride;
   to.cap = p->capacity; to.tile_count = g.tile_count; to.tile_ovf = g.tile_ovf; to.tile_base = ts.tile_base;
   to.region = g.region; to.ovf_area = g.ovf_area; to.ovf_cap = L.ovf_cap; to.rows = g.rows; to.tot = ts.tot;
   to.seg_stride = p->capacity; to.pixel_major = canon ? 0 : 1;

@@ -126,7 +126,8 @@ struct TileScanArgs {
   int64_t* out_dropped;
   const int64_t* bad;
   const int64_t* err;         // K1 errors -> out_dropped = -2 (corrupt level)
-  int gt;
+  int gt;                     // tiles per group (histogram row, K2 CTA)
+  int rows_stride;            // groups per segment in the rows array (>= ngroups)
   // regeneration of tiles K1 could not store (tile_ovf == kTileRedo, or
   // >= ovf_lim once regenerated): k_group_hist, when ovf_cursor[seg] > ovf_lim
   int64_t ovf_lim;
@@ -175,6 +176,7 @@ struct TileOrderArgs {
   const int64_t* seg_tbase;
   const int64_t* bad;
   int gt;
+  int rows_stride;            // as TileScanArgs
 };
 
 // Voxel grid of one stream's window straight from a step's per-tile key
@@ -201,6 +203,7 @@ cudaError_t launch_step_voxel(const StepVoxArgs& a, cudaStream_t st);
 cudaError_t launch_step_hist(const StepVoxArgs& a, int S, int64_t lo, int64_t hi, int64_t* out, cudaStream_t st);
 cudaError_t launch_group_hist(const TileScanArgs& a, cudaStream_t st);
 cudaError_t launch_tilescan(const TileScanArgs& a, cudaStream_t st);
+int tile_order_chunk_keys(int tile_px, int pixel_major, int bits);  // keys per K2 chunk of that launch
 cudaError_t launch_tile_order(const TileOrderArgs& a, cudaStream_t st);
 
 constexpr int kMaxGroupTiles = 16;  // K1 tiles per histogram row / per K2 CTA (runtime gt <= this)

@@ -187,6 +187,10 @@ class StepEngine:
 
         host = torch.cat([self.info.reshape(-1), self.bad]).cpu().numpy()
         nseg = self.info.shape[1]
+        # the next calls' tile groups follow this call's event density (keys_hint:
+        # performance only, the results do not depend on it)
+        if int(host[-1]) == _lib.NO_BAD and nseg:
+            self.params.keys_hint = int(max(0, int(host[:nseg].sum())) // nseg)
         if int(host[-1]) == _lib.NO_BAD and (host[nseg:2 * nseg] == -2).any():
             raise _lib.NativeError("a pixel would cross more than 2**20 thresholds in one frame: an infinite "
                                    "intensity (with validate=False) or a reference level (ref_log) far outside "
@@ -223,6 +227,7 @@ class PipelinedSteps:
             e.params.flags = _lib.EVS_FLAG_DEVICE_CLOCK
             e.params.tick = int(tick)
             e.params.clock_stride = 2
+            e.params.keys_hint = max(x.params.keys_hint for x in self.engines)
         self._tick, self._t0, self._n = int(tick), int(t0), len(windows)
         streams = [torch.cuda.Stream(), torch.cuda.Stream()]
         k1_done = [torch.cuda.Event() for _ in windows]
